@@ -1,0 +1,150 @@
+"""CPU oracle for census + Dual MM with hierarchical minorants (arXiv 1601.06274).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product path (``paper_1601_06274_b200``) never imports it.
+
+This module is argument marshalling (numpy <-> ctypes) over ``dmm_oracle.c``;
+every step of the arithmetic is in that file, which cites PAPER.md per function.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dmm_oracle.c")
+_LIB = os.path.join(_HERE, "libdmm_oracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2, OpenMP) into oracle/libdmm_oracle.so."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "dmm_oracle.h"))
+    ):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra",
+             "-o", tmp, _SRC]
+        )
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        i32, i64 = ctypes.c_int, ctypes.c_int64
+        lib.oracle_census.argtypes = [P, i32, i32, i32, P]
+        lib.oracle_cost_volume.argtypes = [P, P, i32, i32, i32, i32, i32, P]
+        lib.oracle_msg_direct.argtypes = [P, i32, i64, i32, P]
+        lib.oracle_msg.argtypes = [P, i32, i64, i32, P]
+        lib.oracle_min_marginals.argtypes = [P, i32, i32, i64, i32, P]
+        lib.oracle_chain_min.argtypes = [P, i32, i32, i64, i32, P]
+        lib.oracle_chain_min.restype = i64
+        lib.oracle_hm.argtypes = [P, i32, i32, i64, i32, P]
+        lib.oracle_dmm.argtypes = [P, i32, i32, i32, i32, i32, i32, i32, i32, P, P, P, P, P, i32]
+        lib.oracle_energy.argtypes = [P, P, i32, i32, i32, i32, i32, i32]
+        lib.oracle_energy.restype = i64
+        _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def census(img, r: int = 2) -> np.ndarray:
+    img = _c(img, np.uint8)
+    H, W = img.shape
+    out = np.zeros((H, W), np.uint32)
+    if _load().oracle_census(_p(img), W, H, r, _p(out)):
+        raise ValueError("oracle_census: bad arguments")
+    return out
+
+
+def cost_volume(cl, cr, d_min: int, K: int, oob: int = 12) -> np.ndarray:
+    cl, cr = _c(cl, np.uint32), _c(cr, np.uint32)
+    H, W = cl.shape
+    D = np.zeros((H, W, K), np.uint8)
+    if _load().oracle_cost_volume(_p(cl), _p(cr), W, H, d_min, K, oob, _p(D)):
+        raise ValueError("oracle_cost_volume: bad arguments")
+    return D
+
+
+def msg(a, ws: int, T: int, direct: bool = False) -> np.ndarray:
+    a = _c(a, np.int64)
+    out = np.zeros_like(a)
+    fn = _load().oracle_msg_direct if direct else _load().oracle_msg
+    fn(_p(a), a.shape[0], ws, T, _p(out))
+    return out
+
+
+def min_marginals(F, ws: int, T: int) -> np.ndarray:
+    F = _c(F, np.int64)
+    n, K = F.shape
+    m = np.zeros_like(F)
+    _load().oracle_min_marginals(_p(F), n, K, ws, T, _p(m))
+    return m
+
+
+def chain_min(F, ws: int, T: int):
+    F = _c(F, np.int64)
+    n, K = F.shape
+    x = np.zeros(n, np.int32)
+    v = _load().oracle_chain_min(_p(F), n, K, ws, T, _p(x))
+    return int(v), x
+
+
+def hm(F, ws: int, T: int) -> np.ndarray:
+    F = _c(F, np.int64)
+    n, K = F.shape
+    lam = np.zeros_like(F)
+    _load().oracle_hm(_p(F), n, K, ws, T, _p(lam))
+    return lam
+
+
+def dmm(D, w_h: int, w_v: int, T: int, Fbits: int, iters: int, nthreads: int = 1):
+    """Returns dict(fdual, gdual, labels, bound_hist, energy) (all exact ints)."""
+    D = _c(D, np.uint8)
+    H, W, K = D.shape
+    f = np.zeros((H, W, K), np.int64)
+    g = np.zeros((H, W, K), np.int64)
+    lab = np.zeros((H, W), np.int32)
+    bh = np.zeros(2 * max(iters, 1), np.int64)
+    e = np.zeros(1, np.int64)
+    rc = _load().oracle_dmm(_p(D), W, H, K, w_h, w_v, T, Fbits, iters, _p(f), _p(g), _p(lab),
+                            _p(bh), _p(e), nthreads)
+    if rc:
+        raise ValueError("oracle_dmm: bad arguments")
+    return dict(fdual=f, gdual=g, labels=lab, bound_hist=bh, energy=int(e[0]))
+
+
+def energy(D, labels, w_h: int, w_v: int, T: int) -> int:
+    D = _c(D, np.uint8)
+    labels = _c(labels, np.int32)
+    H, W, K = D.shape
+    return int(_load().oracle_energy(_p(D), _p(labels), W, H, K, w_h, w_v, T))
+
+
+def solve(left, right, d_min: int, K: int, w: int = 3, T: int = 4, Fbits: int = 4,
+          iters: int = 4, r: int = 2, oob: int | None = None, nthreads: int = 1):
+    """Whole path on the CPU: census x2 -> cost volume -> DMM."""
+    if oob is None:
+        oob = ((2 * r + 1) ** 2 - 1) // 2
+    cl, cr = census(left, r), census(right, r)
+    D = cost_volume(cl, cr, d_min, K, oob)
+    out = dmm(D, w, w, T, Fbits, iters, nthreads)
+    out.update(codes_left=cl, codes_right=cr, D=D)
+    return out

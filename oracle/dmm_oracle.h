@@ -1,0 +1,88 @@
+/*
+ * dmm_oracle.h -- plain, slow, obviously-correct CPU oracle for the hot path of
+ * arXiv 1601.06274 (Shekhovtsov, Reinbacher, Graber, Pock, CVWW 2016):
+ * census cost volume + Dual MM (Algorithm 2) with hierarchical minorants
+ * (Handshake, Algorithm 5).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py may load this library.
+ * It shares no code, header, table or constant generator with the CUDA path
+ * (paper_1601_06274_b200/csrc), and neither side includes the other.
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n (+ section / equation).
+ * Readings of silent or garbled passages are listed in DESIGN.md "Readings".
+ *
+ * All cost arithmetic is exact integer (int64).  Energies / bounds are in
+ * units of 2^-Fbits (fixed point), reading R9.
+ * Layouts: images / codes / labels are row-major [H][W]; cost volumes and
+ * duals are label-contiguous [H][W][K] (dense, no padding).
+ *
+ * Parity status: every function below is pinned by tests/test_oracle_*.py
+ * (brute force, closed forms, paper-printed values); none is "parity unpinned".
+ */
+#ifndef DMM_ORACLE_H
+#define DMM_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Census transform (Sec. 3.1; reading R17): bit b, in raster order over
+ * the (2r+1)^2 window offsets skipping the centre, is [I(nbr) < I(centre)];
+ * neighbours outside the image replicate the border.  r in {1,2}.
+ * Returns 0, or 1 on bad arguments. */
+int oracle_census(const uint8_t* img, int W, int H, int r, uint32_t* codes);
+
+/* Hamming cost volume ("f_i(x_i) = D_i(u(x_i))"):
+ * D[y][x][k] = popcount(cl[y][x] ^ cr[y][x-d_k]), d_k = d_min + k,
+ * or oob when x-d_k is outside [0,W).  Returns 0 / 1 (bad args). */
+int oracle_cost_volume(const uint32_t* cl, const uint32_t* cr, int W, int H,
+                       int d_min, int K, int oob, uint8_t* D);
+
+/* Message passing, definition (P:663-667 Eq. msg-pass; Msg in Alg.5):
+ * out(b) = min_a a(a) + ws*min(|a-b|, T), by direct O(K^2) enumeration. */
+void oracle_msg_direct(const int64_t* a, int K, int64_t ws, int T, int64_t* out);
+
+/* Same message by the O(K) lower-envelope distance transform for the
+ * truncated-linear term (forward pass, backward pass, min with min(a)+ws*T). */
+void oracle_msg(const int64_t* a, int K, int64_t ws, int T, int64_t* out);
+
+/* Min-marginals of a chain (Def. P:631-636, Eq. P:646-649):
+ * m_i = phi_{i-1,i} + F_i + phi_{i+1,i}.  F, m are [n][K]. */
+void oracle_min_marginals(const int64_t* F, int n, int K, int64_t ws, int T, int64_t* m);
+
+/* Chain optimum min_x sum_i F_i(x_i) + sum ws*min(|x_i-x_{i+1}|,T) by plain
+ * Viterbi (never calls the minorant code).  x_opt (nullable) receives the
+ * lexicographically smallest optimal labelling. */
+int64_t oracle_chain_min(const int64_t* F, int n, int K, int64_t ws, int T, int32_t* x_opt);
+
+/* Hierarchical minorant of one chain (Handshake Alg.5 P:811-830,
+ * schedule Fig.11), reading R5/R7/R8/R9/R10 of DESIGN.md.
+ * lam is [n][K]. */
+void oracle_hm(const int64_t* F, int n, int K, int64_t ws, int T, int64_t* lam);
+
+/* Dual MM (Algorithm 2) on the 4-connected grid with all unaries in
+ * the horizontal subproblem f and vertical pairwise in g (reading R3), initial
+ * g_ = 0 (R4), `iters` full iterations (H half-step then V half-step, R5).
+ *   D       u8 [H][W][K] cost volume (unscaled).
+ *   pairwise f_ij = w * min(|a-b|, T) (w = w_h or w_v), all scaled by 2^Fbits.
+ *   fdual, gdual (nullable): int64 [H][W][K], the minorants f_, g_ after the
+ *     last H resp. V half-step of the last iteration.
+ *   labels (nullable): int32 [H][W], lowest-index argmin of the last V
+ *     minorant (R13, R14).
+ *   bound_hist (nullable): int64 [2*iters], b_{2t} after H, b_{2t+1} after V.
+ *   energy (nullable): E(labels) * 2^Fbits.
+ * nthreads <= 1 runs single-threaded.  Returns 0, or 1 on bad arguments. */
+int oracle_dmm(const uint8_t* D, int W, int H, int K, int w_h, int w_v, int T,
+               int Fbits, int iters, int64_t* fdual, int64_t* gdual,
+               int32_t* labels, int64_t* bound_hist, int64_t* energy, int nthreads);
+
+/* Primal energy Eq.3 of a labelling, unscaled:
+ * sum_i D_i(x_i) + w_h sum_h min(|x_i-x_j|,T) + w_v sum_v min(|x_i-x_j|,T). */
+int64_t oracle_energy(const uint8_t* D, const int32_t* labels, int W, int H, int K,
+                      int w_h, int w_v, int T);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
