@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: census cost volume + Dual MM (4 iterations) at the
+KITTI shape 1242x375x128 (BASELINE.json configs[1]), one frame per GPU per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = census x2 + cost volume + `iters` Dual MM iterations (H and V
+half-steps) + labelling + primal energy + dual bounds, on synthetic
+warped-texture input resident in HBM.  Metric: cost-volume cell-iterations/s
+= W*H*K*iters*frames / step time (whole job, all ranks).  One JSON line on rank 0.
+Multi-GPU (torchrun): every rank solves its own frame (frame sharding, weak
+scaling, no data-path collective); timing is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+METRIC = "cost-volume cell-iterations/s (1242x375x128, 4 dual iterations)"
+UNIT = "cell-iter/s"
+W_REG, T_REG, FBITS = 3, 4, 4           # pairwise w, truncation T, fixed-point bits (DESIGN R2, R9)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def traffic_per_launch():
+    """dram__bytes_read.sum + dram__bytes_write.sum per hm_kernel launch from the
+    committed ncu --set full capture summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("hm_kernel_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_sample(left, right, K, iters, nthreads, rows=None):
+    """Time the CPU oracle (as it stands) on a bounded sample; returns
+    (cell-iter/s, seconds, description)."""
+    import oracle
+    oracle.build()
+    if rows is not None:
+        left, right = left[:rows], right[:rows]
+    H, W = left.shape
+    t0 = time.perf_counter()
+    oracle.solve(left, right, 0, K, W_REG, T_REG, FBITS, iters, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    desc = (f"oracle (C, OpenMP over chains) census+cost+{iters} DMM iteration(s)+energy on "
+            f"{W}x{H}x{K} ({'first %d rows of ' % rows if rows else ''}the step's frame), "
+            f"{nthreads} threads")
+    return W * H * K * iters / dt, dt, desc
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the host cores, same config,
+    metric and unit; each step is a bounded sample (first 32 rows of the frame,
+    all iterations).  Rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    c = datagen.CONFIGS[args.config]
+    W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+    left, right, _ = datagen.pair(c["kind"], W, H, K, seed=0)
+    nth = os.cpu_count() or 1
+    rows = 32
+    for _ in range(args.warmup):
+        cpu_oracle_sample(left, right, K, iters, nth, rows)
+    times = []
+    desc = ""
+    for _ in range(args.steps):
+        v, dt, desc = cpu_oracle_sample(left, right, K, iters, nth, rows)
+        times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = W * rows * K * iters / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: stereo {W}x{H}, {K} disparities, census 5x5, {iters} dual iterations "
+                               f"(reference arm: bounded sample of the first {rows} rows per step)",
+                   "W": W, "H": H, "K": K, "iters": iters, "sample_rows": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1601_06274_b200 as dmm
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c = datagen.CONFIGS[args.config]
+    W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+    left, right, _ = datagen.pair(c["kind"], W, H, K, seed=rank)   # one frame per rank
+    ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
+                      max_iters=iters, device=dev)
+    lt = torch.from_numpy(left).to(dev)
+    rt = torch.from_numpy(right).to(dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ctx.cost_volume(lt, rt, stream=stream)
+        ctx.solve(iters, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    # L2 (126 MB) is flushed between timed steps by overwriting a 256 MB buffer
+    # outside the timed events; the step's own working set (~1.0 GB) exceeds L2.
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ctx.read_profile()
+    ctx.set_profiling(True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count - launches0
+    clocks = sampler.stop()
+    ctx.set_profiling(False)
+    prof = ctx.read_profile()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    e, b, hist = ctx.result()
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    cells = W * H * K
+    value = world * cells * iters / (ms / 1e3)
+
+    # roofline of the dominant kernel family: hm_kernel (H and V half-steps)
+    hbm, peak_kind = peaks()
+    ms_h, n_h = prof["hm_h"]
+    ms_v, n_v = prof["hm_v"]
+    alg_bytes_per_step = cells * (5 + 9 * (iters - 1) + 8 * iters)
+    achieved = alg_bytes_per_step * args.steps / ((ms_h + ms_v) / 1e3) / 1e9
+    tr = traffic_per_launch()
+    step_ms_prof = sum(v[0] for v in prof.values()) / args.steps
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": tr, "kernel": "hm_kernel (H+V half-steps)", "peak_kind": peak_kind,
+                "launches": n_h + n_v,
+                "alg_bytes_per_launch": alg_bytes_per_step / (2 * iters),
+                "share_of_step": (ms_h + ms_v) / args.steps / step_ms_prof if step_ms_prof else None,
+                "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()}}
+
+    # end to end through the public C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        lh = torch.from_numpy(left).pin_memory()
+        rh = torch.from_numpy(right).pin_memory()
+        lab = torch.empty((H, W), dtype=torch.uint8).pin_memory()
+        for _ in range(2):
+            ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall_ms = (time.perf_counter() - w0) * 1e3 / args.steps
+        ems = max(t0.elapsed_time(t1) / args.steps, wall_ms)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": world * cells * iters / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * W * H, "d2h_bytes_per_step": W * H + 8 + 16 * iters,
+               "ms_per_step": ems}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nth = os.cpu_count() or 1
+        v, dt, desc = cpu_oracle_sample(left, right, K, 2, nth)
+        cpu = {"value": v, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc, "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: stereo {W}x{H}, {K} disparities, census 5x5, "
+                                   f"{iters} dual iterations, warped-texture pair, 1 frame per GPU",
+                       "W": W, "H": H, "K": K, "iters": iters, "w": W_REG, "T": T_REG, "frac_bits": FBITS,
+                       "fps": world / (ms / 1e3), "parallelism": f"frames x{world}",
+                       "l2": "flushed between timed steps (256 MB write outside events); step working set ~1 GB"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "result": {"energy": e / (1 << FBITS), "bound": b / (1 << FBITS)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

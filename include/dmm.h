@@ -1,0 +1,137 @@
+/*
+ * dmm.h -- C ABI of the B200 (sm_100a) hot path of arXiv 1601.06274
+ * (Shekhovtsov, Reinbacher, Graber, Pock, "Solving Dense Image Matching in
+ * Real-Time using Discrete-Continuous Optimization", CVWW 2016):
+ *
+ *   census transform -> Hamming cost volume -> K iterations of Dual MM
+ *   (Algorithm 2) with hierarchical (Handshake) minorants -> labelling,
+ *   primal energy, dual bound.
+ *
+ * Citations "P:n" are lines of the paper text with the section /
+ * equation / algorithm they fall in; readings of silent or garbled passages are
+ * numbered R1..R21 in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - extern "C", never throw, return dmm_status (DMM_OK == 0).
+ *  - Device pointers are CUDA global-memory pointers on the context's device;
+ *    host pointers are ordinary (preferably pinned) host memory.
+ *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ *    Every call is stream-ordered and asynchronous unless it says "synchronises".
+ *  - Ownership: the caller owns images, outputs and the device workspace
+ *    (allocate with dmm_workspace_bytes()); the context owns only small host
+ *    state.  A context is single-threaded; distinct contexts are independent.
+ *  - Integers are exact.  Costs, bounds and energies are int64 in units of
+ *    2^-frac_bits (fixed point, reading R9); E(x) is an integer times 2^F.
+ *  - Layouts: images / labels row-major [H][W] (u8); cost volume and duals are
+ *    exported label-contiguous and dense: [H][W][K].
+ *  - Errors: DMM_E_ARG invalid argument / config, DMM_E_SHAPE pitch < width,
+ *    DMM_E_STATE solve before cost volume / result before solve,
+ *    DMM_E_CUDA a CUDA runtime error (text in dmm_last_error()).
+ */
+#ifndef DMM_B200_H
+#define DMM_B200_H
+#include <stddef.h>
+#include <stdint.h>
+#if defined(__GNUC__)
+#define DMM_API __attribute__((visibility("default")))
+#else
+#define DMM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DMM_OK = 0,
+    DMM_E_ARG = 1,
+    DMM_E_SHAPE = 2,
+    DMM_E_STATE = 3,
+    DMM_E_CUDA = 4,
+    DMM_E_RANGE = 6
+} dmm_status;
+
+typedef struct dmm_config {
+    int32_t width, height;   /* >= 1 each; the grid of P:145-152 (4-connected)        */
+    int32_t d_min, d_max;    /* disparity range; K = d_max - d_min + 1 in [1, 256]       */
+    int32_t census_radius;   /* 1 (3x3, 8 bits) or 2 (5x5, 24 bits), R17         */
+    int32_t w_h, w_v;        /* pairwise weights >= 0: f_ij = w * min(|a-b|, trunc)      */
+    int32_t trunc;           /* T >= 1 (T = 1 is Potts); Fig.2 P:132-142 with eps = 1, R2 */
+    int32_t frac_bits;       /* F in [0, 8]: fixed-point fractional bits (R9)            */
+    int32_t oob_cost;        /* cost when x - d leaves the image; -1 => ((2r+1)^2-1)/2   */
+    int32_t batch;           /* frames held by the context, >= 1 (C5 throughput mode)    */
+    int32_t max_iters;       /* capacity of the per-frame bound history, >= 1            */
+} dmm_config;
+
+typedef struct dmm_ctx dmm_ctx;
+
+/* Bytes of device workspace a context with this config needs (0 if invalid). */
+DMM_API size_t dmm_workspace_bytes(const dmm_config* cfg);
+
+/* Bind a context to caller-owned device memory `workspace` (>= the size above,
+ * 256-byte aligned) on CUDA device `device`.  *out receives the context. */
+DMM_API dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int device,
+                      dmm_ctx** out);
+DMM_API void dmm_destroy(dmm_ctx* ctx);
+
+/* Census codes of both images and the cost volume
+ *   D[y][x][k] = popcount(cL(x,y) ^ cR(x - d_k, y)), d_k = d_min + k
+ * (P:416 Hamming distance; P:161 f_i(x_i) = D_i(u(x_i)); R17, R18),
+ * out-of-image samples = oob_cost.  left/right: device u8 images, row pitch
+ * `pitch` bytes (>= width) of frame `frame`. */
+DMM_API dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right,
+                           int64_t pitch, void* stream);
+
+/* Dual MM (Algorithm 2): g_ := 0 (R4), then `iterations` times
+ * H half-step (per row: h = HM(D*2^F + g_), f_ = h - g_) and V half-step (per
+ * column: v = HM(f_), g_ = v - f_), HM = hierarchical minorant (P:809-856,
+ * Handshake Alg.5).  The last V half-step writes the labelling
+ * (lowest-index argmin of v, R13/R14) and every half step adds its dual bound
+ * sum_chains min (Eq.7) to the history; finally the primal energy of
+ * the labelling (Eq.3) is evaluated on the device.  Frames
+ * [frame, frame+nframes) are solved in the same launches.
+ * 1 <= iterations <= max_iters.  Asynchronous. */
+DMM_API dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, void* stream);
+
+/* Read back the primal energy of the labelling (Eq.3, scaled by 2^F)
+ * and the dual bound b_{2K-1} plus the history b_0..b_{2K-1} (each nullable;
+ * the history has 2*iterations entries).  Synchronises `stream`. */
+DMM_API dmm_status dmm_result(dmm_ctx* ctx, int frame, int64_t* energy, int64_t* bound,
+                      int64_t* bound_history, void* stream);
+
+/* Device copy of the labelling: u8 [H][W] label indices (disparity = d_min + label). */
+DMM_API dmm_status dmm_copy_labels(dmm_ctx* ctx, int frame, uint8_t* labels, void* stream);
+
+/* Parity taps (device destinations): census codes (which 0 = left, 1 = right;
+ * u32 [H][W]); cost volume u8 [H][W][K]; duals int32 [H][W][K] (which 0 = f_
+ * after the last H half-step, 1 = g_ after the last V half-step). */
+DMM_API dmm_status dmm_copy_codes(dmm_ctx* ctx, int frame, int which, uint32_t* dst, void* stream);
+DMM_API dmm_status dmm_copy_cost_volume(dmm_ctx* ctx, int frame, uint8_t* dst, void* stream);
+DMM_API dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void* stream);
+
+/* End-to-end call with HOST buffers: copies both images host->device, runs
+ * dmm_cost_volume + dmm_solve + energy, copies the labelling (u8 [H][W]) and
+ * the scalars back.  Synchronises `stream`. */
+DMM_API dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host,
+                        const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
+                        int64_t* energy, int64_t* bound, void* stream);
+
+/* Number of kernels this context has launched since creation. */
+DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
+
+/* Per-kernel device timing with CUDA events recorded on the launching stream
+ * around every kernel (enable != 0).  dmm_read_profile synchronises the
+ * recorded events, writes per-class totals (ms[c], launches[c]) for the
+ * classes c = 0 census, 1 cost volume, 2 H half-step, 3 V half-step,
+ * 4 energy (arrays of DMM_PROFILE_CLASSES entries) and clears the record. */
+#define DMM_PROFILE_CLASSES 5
+DMM_API dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable);
+DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches);
+
+DMM_API const char* dmm_status_str(dmm_status s);
+DMM_API const char* dmm_last_error(const dmm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,236 @@
+"""B200-native (sm_100a) hot path of arXiv 1601.06274: census cost volume + Dual MM
+with hierarchical minorants.
+
+This module is the thin Python face of the C ABI in ``include/dmm.h``
+(``_lib/libdmm_b200.so``): argument marshalling only.  Every step of the path
+runs in the CUDA kernels of ``csrc/``; PyTorch provides device memory (the
+workspace), streams and ``torch.distributed``.  There is no CPU fallback: if the
+shared library or a CUDA device is missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["Context", "DmmError", "library_path", "load_library", "EXPORTS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_lib", "libdmm_b200.so")
+_lib = None
+
+# every entry point declared in include/dmm.h
+EXPORTS = (
+    "dmm_workspace_bytes", "dmm_create", "dmm_destroy", "dmm_cost_volume", "dmm_solve",
+    "dmm_result", "dmm_copy_labels", "dmm_copy_codes", "dmm_copy_cost_volume", "dmm_copy_dual",
+    "dmm_run_host", "dmm_launch_count", "dmm_status_str", "dmm_last_error",
+    "dmm_set_profiling", "dmm_read_profile",
+)
+PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
+
+
+class DmmError(RuntimeError):
+    pass
+
+
+class DmmConfig(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "width", "height", "d_min", "d_max", "census_radius", "w_h", "w_v", "trunc",
+        "frac_bits", "oob_cost", "batch", "max_iters")]
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libdmm_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} missing: run __graft_entry__.build() "
+                          "(python -m paper_1601_06274_b200._build)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    C = ctypes.POINTER(DmmConfig)
+    sig = {
+        "dmm_workspace_bytes": (ctypes.c_size_t, [C]),
+        "dmm_create": (ctypes.c_int, [C, P, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(P)]),
+        "dmm_destroy": (None, [P]),
+        "dmm_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P, i64, P]),
+        "dmm_solve": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, i32, P]),
+        "dmm_result": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P]),
+        "dmm_copy_labels": (ctypes.c_int, [P, ctypes.c_int, P, P]),
+        "dmm_copy_codes": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P]),
+        "dmm_copy_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P]),
+        "dmm_copy_dual": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P]),
+        "dmm_run_host": (ctypes.c_int, [P, ctypes.c_int, P, P, i32, P, P, P, P]),
+        "dmm_launch_count": (i64, [P]),
+        "dmm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
+        "dmm_last_error": (ctypes.c_char_p, [P]),
+        "dmm_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
+        "dmm_read_profile": (ctypes.c_int, [P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Context:
+    """One problem shape (W x H, disparities d_min..d_max) and `batch` frames.
+
+    Energies / bounds are returned as exact ints in units of 2**-frac_bits
+    (``value / 2**frac_bits`` is the real-valued energy of Eq.3)."""
+
+    def __init__(self, width: int, height: int, d_min: int = 0, d_max: int = 127, w: int = 3,
+                 T: int = 4, frac_bits: int = 4, census_radius: int = 2, oob_cost: int = -1,
+                 batch: int = 1, max_iters: int = 16, w_h: int | None = None,
+                 w_v: int | None = None, device=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise DmmError("no CUDA device: the DMM hot path has no CPU fallback")
+        self._lib = load_library()
+        self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
+        self.cfg = DmmConfig(width, height, d_min, d_max, census_radius,
+                             w if w_h is None else w_h, w if w_v is None else w_v, T, frac_bits,
+                             oob_cost, batch, max_iters)
+        self.W, self.H, self.K = width, height, d_max - d_min + 1
+        self.batch, self.frac_bits, self.max_iters = batch, frac_bits, max_iters
+        nbytes = self._lib.dmm_workspace_bytes(ctypes.byref(self.cfg))
+        if nbytes == 0:
+            raise DmmError("invalid dmm_config")
+        self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) & ~255
+        h = ctypes.c_void_p()
+        self._check(self._lib.dmm_create(ctypes.byref(self.cfg), ctypes.c_void_p(aligned), nbytes,
+                                         self.device.index, ctypes.byref(h)), None)
+        self._h = h
+        self._iters = [0] * batch
+
+    # ---------------------------------------------------------------- plumbing
+    def _check(self, st: int, h):
+        if st != 0:
+            msg = self._lib.dmm_status_str(st).decode()
+            if h is not None:
+                msg += ": " + self._lib.dmm_last_error(h).decode()
+            raise DmmError(msg)
+
+    def _call(self, name, *args):
+        self._check(getattr(self._lib, name)(self._h, *args), self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.dmm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self) -> int:
+        return int(self._lib.dmm_launch_count(self._h))
+
+    def set_profiling(self, enable: bool = True):
+        """Record CUDA events around every kernel launch (on its stream)."""
+        self._call("dmm_set_profiling", 1 if enable else 0)
+
+    def read_profile(self):
+        """{class: (total_ms, launches)} since the last read (synchronises)."""
+        n = len(PROFILE_CLASSES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        self._call("dmm_read_profile", ms, cnt)
+        return {c: (float(ms[i]), int(cnt[i])) for i, c in enumerate(PROFILE_CLASSES)}
+
+    # ------------------------------------------------------------------- path
+    def cost_volume(self, left, right, frame: int = 0, stream=None):
+        """left/right: torch.uint8 (H, W) (row pitch allowed) on this device."""
+        for t in (left, right):
+            if t.dtype.itemsize != 1 or t.device != self.device or t.dim() != 2 or t.stride(1) != 1:
+                raise DmmError("images must be uint8 (H, W) row-major tensors on the context device")
+            if tuple(t.shape) != (self.H, self.W):
+                raise DmmError(f"image shape {tuple(t.shape)} != {(self.H, self.W)}")
+        if left.stride(0) != right.stride(0):
+            raise DmmError("left/right row pitch differ")
+        self._call("dmm_cost_volume", frame, ctypes.c_void_p(left.data_ptr()),
+                   ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream))
+
+    def solve(self, iterations: int = 4, frame: int = 0, nframes: int = 1, stream=None):
+        self._call("dmm_solve", frame, nframes, iterations, _stream_handle(stream))
+        for f in range(frame, frame + nframes):
+            self._iters[f] = iterations
+
+    def result(self, frame: int = 0, stream=None):
+        """(energy, bound, bound_history) as exact ints scaled by 2**frac_bits."""
+        it = self._iters[frame]
+        e = ctypes.c_int64()
+        b = ctypes.c_int64()
+        hist = (ctypes.c_int64 * max(2 * it, 1))()
+        self._call("dmm_result", frame, ctypes.byref(e), ctypes.byref(b), hist, _stream_handle(stream))
+        return int(e.value), int(b.value), [int(v) for v in hist[: 2 * it]]
+
+    def labels(self, frame: int = 0, stream=None):
+        import torch
+        out = torch.empty((self.H, self.W), dtype=torch.uint8, device=self.device)
+        self._call("dmm_copy_labels", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        return out
+
+    def codes(self, which: int, frame: int = 0, stream=None):
+        import torch
+        out = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
+        self._call("dmm_copy_codes", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        return out
+
+    def cost_volume_tensor(self, frame: int = 0, stream=None):
+        import torch
+        out = torch.empty((self.H, self.W, self.K), dtype=torch.uint8, device=self.device)
+        self._call("dmm_copy_cost_volume", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        return out
+
+    def dual(self, which: int, frame: int = 0, stream=None):
+        """which 0: f_ after the last H half-step; 1: g_ after the last V half-step."""
+        import torch
+        out = torch.empty((self.H, self.W, self.K), dtype=torch.int32, device=self.device)
+        self._call("dmm_copy_dual", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        return out
+
+    def run_host(self, left, right, iterations: int = 4, labels_out=None, frame: int = 0, stream=None):
+        """End-to-end through the C ABI with HOST buffers (numpy or CPU tensors,
+        preferably pinned): H2D, cost volume, solve, energy, D2H.  Returns
+        (labels_host, energy, bound)."""
+        import torch
+
+        def host_ptr(a):
+            if isinstance(a, np.ndarray):
+                a = np.ascontiguousarray(a, dtype=np.uint8)
+                return a, a.ctypes.data
+            if a.device.type != "cpu" or not a.is_contiguous():
+                raise DmmError("run_host expects contiguous host buffers")
+            return a, a.data_ptr()
+
+        l, lp = host_ptr(left)
+        r, rp = host_ptr(right)
+        if labels_out is None:
+            labels_out = torch.empty((self.H, self.W), dtype=torch.uint8).pin_memory()
+        _, op = host_ptr(labels_out)
+        e = ctypes.c_int64()
+        b = ctypes.c_int64()
+        self._call("dmm_run_host", frame, ctypes.c_void_p(lp), ctypes.c_void_p(rp), iterations,
+                   ctypes.c_void_p(op), ctypes.byref(e), ctypes.byref(b), _stream_handle(stream))
+        self._iters[frame] = iterations
+        return labels_out, int(e.value), int(b.value)

@@ -1,0 +1,364 @@
+// capi.cu -- the extern "C" boundary declared in include/dmm.h: argument
+// checks, workspace carving, kernel orchestration of Algorithm 2,
+// and error reporting.  No torch types cross this boundary.
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dmm.h"
+#include "dmm_internal.cuh"
+
+struct dmm_ctx {
+    dmm_config cfg;
+    int K, KP, device, oob;
+    dmm::Layout L;
+    char* ws;
+    size_t ws_bytes;
+    // per-frame host state
+    int* has_cost;
+    int* iters_done;
+    long long launches;
+    std::string err;
+    // event profiling (dmm_set_profiling)
+    int profiling;
+    struct Rec { int cls; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+};
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+bool valid(const dmm_config* c) {
+    if (!c) return false;
+    const int K = c->d_max - c->d_min + 1;
+    return c->width >= 1 && c->height >= 1 && c->width <= (1 << 16) && c->height <= (1 << 16) &&
+           K >= 1 && K <= 256 && (c->census_radius == 1 || c->census_radius == 2) &&
+           c->w_h >= 0 && c->w_v >= 0 && c->w_h <= 255 && c->w_v <= 255 && c->trunc >= 1 &&
+           c->frac_bits >= 0 && c->frac_bits <= 8 && c->oob_cost >= -1 && c->oob_cost <= 255 &&
+           c->batch >= 1 && c->max_iters >= 1 && c->max_iters <= 1024;
+}
+
+int kp_of(int K) {
+    int lpl = 1;
+    while (32 * lpl < K) lpl *= 2;
+    return 32 * lpl;
+}
+
+// Byte offsets of every array inside one frame block; returns the block size.
+size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
+    const size_t W = c->width, H = c->height, KP = kp_of(c->d_max - c->d_min + 1);
+    const size_t px = W * H, cells = px * KP;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = align256(o + bytes); return r; };
+    off->img_l = (uint8_t*)take(px);
+    off->img_r = (uint8_t*)take(px);
+    off->codes_l = (uint32_t*)take(4 * px);
+    off->codes_r = (uint32_t*)take(4 * px);
+    off->D = (uint8_t*)take(cells);
+    off->fdual = (int32_t*)take(4 * cells);
+    off->gdual = (int32_t*)take(4 * cells);
+    off->fwd = (int32_t*)take(4 * cells);
+    off->bwd = (int32_t*)take(4 * cells);
+    off->labels = (uint8_t*)take(px);
+    off->bounds = (long long*)take(8 * 2 * (size_t)c->max_iters);
+    off->energy = (long long*)take(8);
+    return o;
+}
+
+dmm_status cuda_err(dmm_ctx* ctx, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return DMM_OK;
+    if (ctx) ctx->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return DMM_E_CUDA;
+}
+
+dmm_status check_launch(dmm_ctx* ctx, const char* where) {
+    return cuda_err(ctx, cudaGetLastError(), where);
+}
+
+cudaEvent_t get_event(dmm_ctx* c) {
+    if (!c->pool.empty()) { cudaEvent_t e = c->pool.back(); c->pool.pop_back(); return e; }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with events when profiling is on.
+struct Timed {
+    dmm_ctx* c; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
+    Timed(dmm_ctx* c_, int cls_, cudaStream_t s_) : c(c_), cls(cls_), s(s_) {
+        if (c->profiling) { a = get_event(c); cudaEventRecord(a, s); }
+    }
+    ~Timed() {
+        c->launches += 1;
+        if (a) {
+            cudaEvent_t b = get_event(c);
+            cudaEventRecord(b, s);
+            c->recs.push_back({cls, a, b});
+        }
+    }
+};
+
+dmm_status frame_ok(dmm_ctx* ctx, int frame, int n = 1) {
+    if (!ctx || frame < 0 || n < 1 || frame + n > ctx->cfg.batch) {
+        if (ctx) ctx->err = "frame index out of range";
+        return DMM_E_ARG;
+    }
+    return DMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t dmm_workspace_bytes(const dmm_config* cfg) {
+    if (!valid(cfg)) return 0;
+    dmm::FramePtrs off;
+    return frame_layout(cfg, &off) * (size_t)cfg->batch;
+}
+
+dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int device,
+                      dmm_ctx** out) {
+    if (!out || !valid(cfg) || !workspace || ((uintptr_t)workspace & 255)) return DMM_E_ARG;
+    *out = nullptr;
+    if (bytes < dmm_workspace_bytes(cfg)) return DMM_E_ARG;
+    dmm_ctx* c = new (std::nothrow) dmm_ctx();
+    if (!c) return DMM_E_ARG;
+    c->cfg = *cfg;
+    c->K = cfg->d_max - cfg->d_min + 1;
+    c->KP = kp_of(c->K);
+    c->device = device;
+    c->oob = cfg->oob_cost >= 0 ? cfg->oob_cost
+                                : ((2 * cfg->census_radius + 1) * (2 * cfg->census_radius + 1) - 1) / 2;
+    dmm::FramePtrs off;
+    c->L.frame_bytes = frame_layout(cfg, &off);
+    char* b = (char*)workspace;
+    c->L.base.img_l = (uint8_t*)(b + (size_t)off.img_l);
+    c->L.base.img_r = (uint8_t*)(b + (size_t)off.img_r);
+    c->L.base.codes_l = (uint32_t*)(b + (size_t)off.codes_l);
+    c->L.base.codes_r = (uint32_t*)(b + (size_t)off.codes_r);
+    c->L.base.D = (uint8_t*)(b + (size_t)off.D);
+    c->L.base.fdual = (int32_t*)(b + (size_t)off.fdual);
+    c->L.base.gdual = (int32_t*)(b + (size_t)off.gdual);
+    c->L.base.fwd = (int32_t*)(b + (size_t)off.fwd);
+    c->L.base.bwd = (int32_t*)(b + (size_t)off.bwd);
+    c->L.base.labels = (uint8_t*)(b + (size_t)off.labels);
+    c->L.base.bounds = (long long*)(b + (size_t)off.bounds);
+    c->L.base.energy = (long long*)(b + (size_t)off.energy);
+    c->L.W = cfg->width; c->L.H = cfg->height; c->L.K = c->K; c->L.KP = c->KP;
+    c->ws = b;
+    c->ws_bytes = bytes;
+    c->has_cost = new int[cfg->batch]();
+    c->iters_done = new int[cfg->batch]();
+    c->launches = 0;
+    c->profiling = 0;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        dmm_destroy(c);
+        return DMM_E_CUDA;
+    }
+    *out = c;
+    return DMM_OK;
+}
+
+void dmm_destroy(dmm_ctx* ctx) {
+    if (!ctx) return;
+    for (auto& r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : ctx->pool) cudaEventDestroy(e);
+    delete[] ctx->has_cost;
+    delete[] ctx->iters_done;
+    delete ctx;
+}
+
+dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right,
+                           int64_t pitch, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
+    if (pitch < ctx->cfg.width) { ctx->err = "pitch < width"; return DMM_E_SHAPE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, 1, ctx->cfg.census_radius, pitch, left, right, s); }
+    { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, 1, ctx->cfg.d_min, ctx->oob, s); }
+    if ((st = check_launch(ctx, "cost_volume"))) return st;
+    ctx->has_cost[frame] = 1;
+    ctx->iters_done[frame] = 0;
+    return DMM_OK;
+}
+
+dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, void* stream) {
+    dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st) return st;
+    if (iterations < 1 || iterations > ctx->cfg.max_iters) {
+        ctx->err = "iterations must be in [1, max_iters]";
+        return DMM_E_ARG;
+    }
+    for (int f = frame; f < frame + nframes; ++f)
+        if (!ctx->has_cost[f]) { ctx->err = "solve before cost volume"; return DMM_E_STATE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    {   // bound history + energy of every frame: one strided memset
+        dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+        const size_t row = (size_t)((char*)P.energy - (char*)P.bounds) + 8;
+        if ((st = cuda_err(ctx, cudaMemset2DAsync(P.bounds, ctx->L.frame_bytes, 0, row, nframes, s),
+                           "memset bounds")))
+            return st;
+    }
+    const int T = ctx->cfg.trunc < ctx->K ? ctx->cfg.trunc : ctx->K;   // T >= K: untruncated
+    for (int t = 0; t < iterations; ++t) {
+        for (int v = 0; v < 2; ++v) {
+            dmm::PassArgs a;
+            a.L = ctx->L;
+            a.frame0 = frame;
+            a.fbits = ctx->cfg.frac_bits;
+            a.ws = (v ? ctx->cfg.w_v : ctx->cfg.w_h) << ctx->cfg.frac_bits;
+            a.wsT = a.ws * T;
+            a.first = (t == 0 && v == 0);
+            a.last = (t == iterations - 1 && v == 1);
+            a.bound_slot = 2 * t + v;
+            Timed tm(ctx, 2 + v, s);
+            dmm::launch_hm_pass(a, v, nframes, s);
+        }
+    }
+    {
+        Timed tm(ctx, 4, s);
+        dmm::launch_energy(ctx->L, frame, nframes, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc,
+                           ctx->cfg.frac_bits, s);
+    }
+    if ((st = check_launch(ctx, "solve"))) return st;
+    for (int f = frame; f < frame + nframes; ++f) ctx->iters_done[f] = iterations;
+    return DMM_OK;
+}
+
+dmm_status dmm_result(dmm_ctx* ctx, int frame, int64_t* energy, int64_t* bound,
+                      int64_t* bound_history, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    const int it = ctx->iters_done[frame];
+    if (it < 1) { ctx->err = "result before solve"; return DMM_E_STATE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    long long e = 0;
+    if (energy &&
+        (st = cuda_err(ctx, cudaMemcpyAsync(&e, P.energy, 8, cudaMemcpyDeviceToHost, s), "d2h")))
+        return st;
+    long long hist[2 * 1024];
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(hist, P.bounds, 8 * 2 * (size_t)it, cudaMemcpyDeviceToHost, s),
+                       "d2h bounds")))
+        return st;
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
+    if (energy) *energy = e;
+    if (bound) *bound = hist[2 * it - 1];
+    if (bound_history) memcpy(bound_history, hist, 8 * 2 * (size_t)it);
+    return DMM_OK;
+}
+
+dmm_status dmm_copy_labels(dmm_ctx* ctx, int frame, uint8_t* labels, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!labels) return DMM_E_ARG;
+    if (ctx->iters_done[frame] < 1) { ctx->err = "labels before solve"; return DMM_E_STATE; }
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    return cuda_err(ctx,
+                    cudaMemcpyAsync(labels, P.labels, (size_t)ctx->L.W * ctx->L.H,
+                                    cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                    "copy labels");
+}
+
+dmm_status dmm_copy_codes(dmm_ctx* ctx, int frame, int which, uint32_t* dst, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
+    if (!ctx->has_cost[frame]) return DMM_E_STATE;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    return cuda_err(ctx,
+                    cudaMemcpyAsync(dst, which ? P.codes_r : P.codes_l, 4 * (size_t)ctx->L.W * ctx->L.H,
+                                    cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                    "copy codes");
+}
+
+dmm_status dmm_copy_cost_volume(dmm_ctx* ctx, int frame, uint8_t* dst, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!dst) return DMM_E_ARG;
+    if (!ctx->has_cost[frame]) return DMM_E_STATE;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    dmm::launch_unpad_u8(P.D, dst, (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
+    return check_launch(ctx, "copy cost volume");
+}
+
+dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
+    if (ctx->iters_done[frame] < 1) return DMM_E_STATE;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    dmm::launch_unpad_i32(which ? P.gdual : P.fdual, dst, (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP,
+                          (cudaStream_t)stream);
+    return check_launch(ctx, "copy dual");
+}
+
+dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const uint8_t* right_host,
+                        int32_t iterations, uint8_t* labels_host, int64_t* energy, int64_t* bound,
+                        void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!left_host || !right_host || !labels_host) return DMM_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    const size_t px = (size_t)ctx->L.W * ctx->L.H;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(P.img_l, left_host, px, cudaMemcpyHostToDevice, s), "h2d")))
+        return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(P.img_r, right_host, px, cudaMemcpyHostToDevice, s), "h2d")))
+        return st;
+    if ((st = dmm_cost_volume(ctx, frame, P.img_l, P.img_r, ctx->L.W, stream))) return st;
+    if ((st = dmm_solve(ctx, frame, 1, iterations, stream))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(labels_host, P.labels, px, cudaMemcpyDeviceToHost, s), "d2h")))
+        return st;
+    return dmm_result(ctx, frame, energy, bound, nullptr, stream);
+}
+
+int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable) {
+    if (!ctx) return DMM_E_ARG;
+    ctx->profiling = enable != 0;
+    return DMM_OK;
+}
+
+dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches) {
+    if (!ctx) return DMM_E_ARG;
+    for (int c = 0; c < DMM_PROFILE_CLASSES; ++c) {
+        if (ms) ms[c] = 0.0;
+        if (launches) launches[c] = 0;
+    }
+    dmm_status st = DMM_OK;
+    for (auto& r : ctx->recs) {
+        float t = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess && st == DMM_OK) st = cuda_err(ctx, e, "read_profile");
+        if (ms) ms[r.cls] += t;
+        if (launches) launches[r.cls] += 1;
+        ctx->pool.push_back(r.a);
+        ctx->pool.push_back(r.b);
+    }
+    ctx->recs.clear();
+    return st;
+}
+
+const char* dmm_status_str(dmm_status s) {
+    switch (s) {
+        case DMM_OK: return "ok";
+        case DMM_E_ARG: return "invalid argument";
+        case DMM_E_SHAPE: return "shape mismatch";
+        case DMM_E_STATE: return "invalid state";
+        case DMM_E_CUDA: return "CUDA error";
+        case DMM_E_RANGE: return "numeric range";
+    }
+    return "unknown";
+}
+
+const char* dmm_last_error(const dmm_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+}  // extern "C"

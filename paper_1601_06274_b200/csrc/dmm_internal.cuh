@@ -1,0 +1,86 @@
+// dmm_internal.cuh -- device-side layout and parameter blocks shared by the
+// sm_100a kernels of the hot path (census / cost / chain DP / energy).
+//
+// HBM layout of one frame:
+//   codes  u32 [H][W]           census codes, left and right
+//   D      u8  [H][W][KP]       cost volume, label-contiguous, KP = 32*LPL >= K
+//   fdual  i32 [H][W][KP]       f_ (horizontal minorant), written by the H pass
+//   gdual  i32 [H][W][KP]       g_ (vertical minorant),   written by the V pass
+//   fwd    i32 [H][W][KP]       message scratch: message into a node from the left / top
+//   bwd    i32 [H][W][KP]       message scratch: message into a node from the right / bottom
+//   labels u8  [H][W]
+// Both chain orientations read a node's K-vector as one contiguous KP-element
+// run, so H chains (stride KP) and V chains (stride W*KP) are both coalesced.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dmm {
+
+// Labels k >= K (padding up to KP) enter every message as +BIG, so they never
+// win a minimum; BIG + any reachable message value stays far below 2^31.
+constexpr int kBig = 1 << 29;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct FramePtrs {
+    uint8_t* img_l;
+    uint8_t* img_r;
+    uint32_t* codes_l;
+    uint32_t* codes_r;
+    uint8_t* D;
+    int32_t* fdual;
+    int32_t* gdual;
+    int32_t* fwd;
+    int32_t* bwd;
+    uint8_t* labels;
+    long long* bounds;   // [2 * max_iters]
+    long long* energy;   // [1]
+};
+
+// Per-frame pointers are base + frame * stride (bytes).
+struct Layout {
+    FramePtrs base;
+    size_t frame_bytes;
+    int W, H, K, KP;
+};
+
+__host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
+    FramePtrs p = L.base;
+    const size_t o = (size_t)f * L.frame_bytes;
+    p.img_l += o; p.img_r += o;
+    p.codes_l = (uint32_t*)((char*)p.codes_l + o);
+    p.codes_r = (uint32_t*)((char*)p.codes_r + o);
+    p.D += o;
+    p.fdual = (int32_t*)((char*)p.fdual + o);
+    p.gdual = (int32_t*)((char*)p.gdual + o);
+    p.fwd = (int32_t*)((char*)p.fwd + o);
+    p.bwd = (int32_t*)((char*)p.bwd + o);
+    p.labels += o;
+    p.bounds = (long long*)((char*)p.bounds + o);
+    p.energy = (long long*)((char*)p.energy + o);
+    return p;
+}
+
+struct PassArgs {
+    Layout L;
+    int frame0;
+    int fbits;        // F
+    int ws;           // w * 2^F
+    int wsT;          // w * 2^F * T
+    int first;        // H pass of iteration 0: g_ == 0, not read
+    int last;         // V pass of the last iteration: write labels
+    int bound_slot;   // index into bounds[]
+};
+
+// kernels (launchers in the .cu files)
+void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t pitch,
+                   const uint8_t* left, const uint8_t* right, cudaStream_t s);
+void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s);
+void launch_hm_pass(const PassArgs& a, int vertical, int nframes, cudaStream_t s);
+void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
+                   cudaStream_t s);
+void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
+void launch_unpad_i32(const int32_t* src, int32_t* dst, long long cells, int K, int KP,
+                      cudaStream_t s);
+
+}  // namespace dmm

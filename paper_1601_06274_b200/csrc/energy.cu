@@ -1,0 +1,57 @@
+// energy.cu -- primal energy of the labelling (Eq.3, with f_i = D_i
+// and f_ij = w*min(|x_i - x_j|, T)), exact int64, scaled by 2^F; plus
+// the de-padding copies used by the parity taps.
+#include "dmm_internal.cuh"
+
+namespace dmm {
+
+__global__ void __launch_bounds__(256)
+energy_kernel(Layout L, int frame0, int w_h, int w_v, int T, int fbits) {
+    FramePtrs P = frame_ptrs(L, frame0 + blockIdx.y);
+    const int W = L.W, H = L.H, KP = L.KP;
+    long long e = 0;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < W * H; q += gridDim.x * blockDim.x) {
+        const int y = q / W, x = q - y * W;
+        const int l = P.labels[q];
+        e += P.D[(size_t)q * KP + l];
+        if (x + 1 < W) e += (long long)w_h * min(abs(l - (int)P.labels[q + 1]), T);
+        if (y + 1 < H) e += (long long)w_v * min(abs(l - (int)P.labels[q + W]), T);
+    }
+    for (int d = 16; d > 0; d >>= 1) e += __shfl_down_sync(kFull, e, d);
+    __shared__ long long part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.energy), (unsigned long long)(s << fbits));
+    }
+}
+
+void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
+                   cudaStream_t s) {
+    int blocks = (L.W * L.H + 255) / 256;
+    if (blocks > 4 * 148) blocks = 4 * 148;
+    energy_kernel<<<dim3(blocks, nframes), 256, 0, s>>>(L, frame0, w_h, w_v, T, fbits);
+}
+
+template <typename T>
+__global__ void unpad_kernel(const T* __restrict__ src, T* __restrict__ dst, long long cells, int K,
+                             int KP) {
+    const long long n = cells * K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / K;
+        dst[i] = src[c * KP + (i - c * K)];
+    }
+}
+
+void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s) {
+    unpad_kernel<uint8_t><<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
+}
+void launch_unpad_i32(const int32_t* src, int32_t* dst, long long cells, int K, int KP,
+                      cudaStream_t s) {
+    unpad_kernel<int32_t><<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
+}
+
+}  // namespace dmm

@@ -1,0 +1,162 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element, on seeded synthetic inputs.  All arithmetic is integer, so the bar is
+bit-exact for codes, cost volume, duals, labels, bound history and energy
+(north_star: "cost volumes and labellings must match the oracle bit-exactly")."""
+import numpy as np
+import pytest
+
+import datagen
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx(**kw):
+    import paper_1601_06274_b200 as dmm
+    return dmm.Context(**kw)
+
+
+def _run_gpu(left, right, d_min, K, w_h, w_v, T, Fb, iters, r=2, oob=-1):
+    H, W = left.shape
+    ctx = _ctx(width=W, height=H, d_min=d_min, d_max=d_min + K - 1, w_h=w_h, w_v=w_v, T=T,
+               frac_bits=Fb, census_radius=r, oob_cost=oob, max_iters=max(iters, 1))
+    lt = torch.from_numpy(left).cuda()
+    rt = torch.from_numpy(right).cuda()
+    ctx.cost_volume(lt, rt)
+    ctx.solve(iters)
+    e, b, hist = ctx.result()
+    out = dict(
+        codes_left=ctx.codes(0).cpu().numpy().view(np.uint32),
+        codes_right=ctx.codes(1).cpu().numpy().view(np.uint32),
+        D=ctx.cost_volume_tensor().cpu().numpy(),
+        fdual=ctx.dual(0).cpu().numpy(),
+        gdual=ctx.dual(1).cpu().numpy(),
+        labels=ctx.labels().cpu().numpy(),
+        energy=e, bound=b, bound_hist=np.array(hist, np.int64))
+    torch.cuda.synchronize()
+    return out
+
+
+def _run_oracle(orc, left, right, d_min, K, w_h, w_v, T, Fb, iters, r=2, oob=-1, nthreads=4):
+    if oob < 0:
+        oob = ((2 * r + 1) ** 2 - 1) // 2
+    cl, cr = orc.census(left, r), orc.census(right, r)
+    D = orc.cost_volume(cl, cr, d_min, K, oob)
+    out = orc.dmm(D, w_h, w_v, T, Fb, iters, nthreads)
+    out.update(codes_left=cl, codes_right=cr, D=D)
+    return out
+
+
+def _compare(g, o):
+    assert np.array_equal(g["codes_left"], o["codes_left"])
+    assert np.array_equal(g["codes_right"], o["codes_right"])
+    assert np.array_equal(g["D"], o["D"])
+    assert np.array_equal(g["fdual"].astype(np.int64), o["fdual"]), "f_ mismatch"
+    assert np.array_equal(g["gdual"].astype(np.int64), o["gdual"]), "g_ mismatch"
+    assert np.array_equal(g["bound_hist"], o["bound_hist"])
+    assert np.array_equal(g["labels"].astype(np.int32), o["labels"])
+    assert g["energy"] == o["energy"]
+    assert g["bound"] == o["bound_hist"][-1]
+
+
+def test_c1_random_dot(orc):
+    """configs[0]: 64x48 random-dot, 16 disparities, truncated linear, 5 iterations."""
+    c = datagen.CONFIGS["C1"]
+    left, right, _ = datagen.pair(c["kind"], c["W"], c["H"], c["K"], 0)
+    args = (c["d_min"], c["K"], 3, 3, 4, 4, c["iters"])
+    _compare(_run_gpu(left, right, *args), _run_oracle(orc, left, right, *args))
+
+
+CASES = [
+    # (W, H, K, d_min, w_h, w_v, T, Fb, iters, r, kind)
+    (37, 29, 5, 0, 2, 3, 2, 4, 2, 2, "rd"),
+    (100, 20, 33, 0, 3, 3, 4, 4, 3, 2, "rd"),       # ragged K (pads), ragged W
+    (70, 41, 64, -3, 1, 4, 1, 0, 2, 1, "rd"),       # Potts, F = 0, negative d_min, 3x3 census
+    (129, 65, 128, 0, 3, 3, 4, 4, 2, 2, "wt-kitti"),
+    (61, 33, 100, 2, 5, 2, 7, 8, 2, 2, "rd"),       # F = 8
+    (50, 47, 200, 0, 3, 3, 4, 4, 1, 2, "wt-middlebury"),
+    (40, 23, 256, 0, 2, 2, 300, 4, 2, 2, "wt-middlebury"),   # T >= K (untruncated)
+    (300, 7, 32, 0, 0, 0, 4, 4, 2, 2, "rd"),        # w = 0 (WTA)
+    (1, 50, 8, 0, 3, 3, 2, 4, 2, 2, "rd"),          # W = 1
+    (50, 1, 8, 0, 3, 3, 2, 4, 2, 2, "rd"),          # H = 1
+    (1, 1, 1, 0, 3, 3, 1, 4, 1, 2, "rd"),           # single pixel, K = 1
+    (2, 2, 2, 0, 9, 9, 1, 4, 3, 1, "rd"),
+    (1025, 3, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),       # long rows, odd splits
+    (5, 513, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),        # long columns
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}xK{c[2]}" for c in CASES])
+def test_parity_cases(orc, case):
+    W, H, K, d_min, w_h, w_v, T, Fb, iters, r, kind = case
+    left, right, _ = datagen.pair(kind, W, H, K, seed=W * 7 + H)
+    args = (d_min, K, w_h, w_v, T, Fb, iters, r)
+    _compare(_run_gpu(left, right, *args), _run_oracle(orc, left, right, *args))
+
+
+def test_batched_frames_equal_single(orc):
+    """Frames solved in one batched launch equal frames solved one by one."""
+    W, H, K = 90, 40, 24
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, batch=3, max_iters=3)
+    pairs = [datagen.pair("rd", W, H, K, s) for s in range(3)]
+    for f, (l, r, _) in enumerate(pairs):
+        ctx.cost_volume(torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda(), frame=f)
+    ctx.solve(3, frame=0, nframes=3)
+    for f, (l, r, _) in enumerate(pairs):
+        e, b, hist = ctx.result(frame=f)
+        o = _run_oracle(orc, l, r, 0, K, 3, 3, 4, 4, 3)
+        assert np.array_equal(np.array(hist), o["bound_hist"])
+        assert e == o["energy"]
+        assert np.array_equal(ctx.labels(frame=f).cpu().numpy().astype(np.int32), o["labels"])
+
+
+def test_run_host_matches_device_path(orc):
+    W, H, K = 120, 60, 32
+    l, r, _ = datagen.pair("wt-kitti", W, H, K, 5)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, max_iters=4)
+    lab, e, b = ctx.run_host(l, r, 4)
+    o = _run_oracle(orc, l, r, 0, K, 3, 3, 4, 4, 4)
+    assert np.array_equal(lab.numpy().astype(np.int32), o["labels"])
+    assert e == o["energy"] and b == o["bound_hist"][-1]
+
+
+def test_deterministic_repeat():
+    W, H, K = 200, 90, 64
+    l, r, _ = datagen.pair("rd", W, H, K, 9)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=4)
+    outs = []
+    for _ in range(3):
+        ctx.cost_volume(torch.from_numpy(l).cuda(), torch.from_numpy(r).cuda())
+        ctx.solve(4)
+        outs.append((ctx.result(), ctx.labels().cpu().numpy(), ctx.dual(1).cpu().numpy()))
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        assert np.array_equal(o[1], outs[0][1]) and np.array_equal(o[2], outs[0][2])
+
+
+def test_errors():
+    import paper_1601_06274_b200 as dmm
+    ctx = _ctx(width=16, height=8, d_min=0, d_max=7, max_iters=2)
+    with pytest.raises(dmm.DmmError):
+        ctx.solve(1)                       # before the cost volume -> DMM_E_STATE
+    z = torch.zeros((8, 16), dtype=torch.uint8, device="cuda")
+    ctx.cost_volume(z, z)
+    with pytest.raises(dmm.DmmError):
+        ctx.solve(0)                       # iterations = 0 -> DMM_E_ARG
+    with pytest.raises(dmm.DmmError):
+        ctx.solve(3)                       # > max_iters
+    with pytest.raises(dmm.DmmError):
+        dmm.Context(width=16, height=8, d_min=0, d_max=300)   # K > 256
+
+
+@pytest.mark.slow
+def test_c2_full_size(orc):
+    """configs[1] at full size (1242x375x128, 4 iterations), in the launch
+    configuration bench.py times: complete element-by-element comparison."""
+    c = datagen.CONFIGS["C2"]
+    left, right, _ = datagen.pair(c["kind"], c["W"], c["H"], c["K"], 0)
+    args = (c["d_min"], c["K"], 3, 3, 4, 4, c["iters"])
+    g = _run_gpu(left, right, *args)
+    o = _run_oracle(orc, left, right, *args, nthreads=max(1, min(16, __import__("os").cpu_count() or 1)))
+    _compare(g, o)
