@@ -168,6 +168,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--wave-mb", type=float, default=None,
+                    help="L2 wave budget of the chain-DP launches in MiB (0 = one launch; default: library's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -191,6 +193,8 @@ def main():
     left, right, _ = datagen.pair(c["kind"], W, H, K, seed=rank)   # one frame per rank
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
                       max_iters=iters, device=dev)
+    if args.wave_mb is not None:
+        ctx.set_wave_bytes(int(args.wave_mb * (1 << 20)))
     lt = torch.from_numpy(left).to(dev)
     rt = torch.from_numpy(right).to(dev)
     stream = torch.cuda.current_stream(dev)

@@ -116,6 +116,24 @@ DMM_API dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_hos
                         const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
                         int64_t* energy, int64_t* bound, void* stream);
 
+/* ---- chain-DP primitives (no context; device int32 arrays, dense
+ * [count][K], K in [1, 256], ws = w * 2^F >= 0, T >= 1).  They run exactly the
+ * device code of the Dual MM kernels, one warp per K-vector.
+ *
+ * dmm_msg: message passing, Eq. msg-pass / Msg of Alg.5
+ * for the truncated-linear f_ij (Fig.2 with eps = 1, reading R2):
+ *   out[v][b] = min_a a[v][a] + ws * min(|a - b|, T).
+ * dmm_handshake: Alg.5 (readings R9/R10) over one edge ij:
+ *   phi_ji  = Msg(Fj + phiR);  m = phiL + Fi + phi_ji;
+ *   phi_ij  = Msg(floor((m - 2 phi_ji) / 2));  phi_ji' = Msg(-phi_ij);
+ * outputs phi_ij (into j) and phi_ji' (into i).  phiL = message into i from
+ * the left, phiR = message into j from the right. */
+DMM_API dmm_status dmm_msg(const int32_t* a, int32_t* out, int count, int K, int32_t ws, int32_t T,
+                           void* stream);
+DMM_API dmm_status dmm_handshake(const int32_t* Fi, const int32_t* Fj, const int32_t* phiL,
+                                 const int32_t* phiR, int32_t* phi_ij, int32_t* phi_ji, int count,
+                                 int K, int32_t ws, int32_t T, void* stream);
+
 /* Number of kernels this context has launched since creation. */
 DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
 
@@ -127,6 +145,14 @@ DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
 #define DMM_PROFILE_CLASSES 5
 DMM_API dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable);
 DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches);
+
+/* Tuning knobs (no effect on results, which are exact).
+ * DMM_TUNE_WAVE_BYTES: the chains of a half-step are launched in waves whose
+ * node data (F records) total at most `value` bytes, so that a wave's
+ * re-reads across hierarchy levels stay in the 126 MB L2; 0 = one launch.
+ * Default 0 (measured: waves cost more occupancy than they save in L2 misses). */
+#define DMM_TUNE_WAVE_BYTES 1
+DMM_API dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value);
 
 DMM_API const char* dmm_status_str(dmm_status s);
 DMM_API const char* dmm_last_error(const dmm_ctx* ctx);

@@ -25,8 +25,9 @@ EXPORTS = (
     "dmm_workspace_bytes", "dmm_create", "dmm_destroy", "dmm_cost_volume", "dmm_solve",
     "dmm_result", "dmm_copy_labels", "dmm_copy_codes", "dmm_copy_cost_volume", "dmm_copy_dual",
     "dmm_run_host", "dmm_launch_count", "dmm_status_str", "dmm_last_error",
-    "dmm_set_profiling", "dmm_read_profile",
+    "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
 )
+TUNE_WAVE_BYTES = 1
 PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
 
 
@@ -72,6 +73,9 @@ def load_library():
         "dmm_last_error": (ctypes.c_char_p, [P]),
         "dmm_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
         "dmm_read_profile": (ctypes.c_int, [P, P, P]),
+        "dmm_set_tuning": (ctypes.c_int, [P, ctypes.c_int, i64]),
+        "dmm_msg": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, i32, i32, P]),
+        "dmm_handshake": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, i32, i32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -85,6 +89,35 @@ def _stream_handle(stream) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+def _prim_check(st):
+    if st != 0:
+        raise DmmError(load_library().dmm_status_str(st).decode())
+
+
+def msg(a, ws: int, T: int, stream=None):
+    """Device Msg (Eq. msg-pass) on int32 CUDA tensor a[count, K]."""
+    import torch
+    a = a.contiguous()
+    out = torch.empty_like(a)
+    count, K = a.shape
+    _prim_check(load_library().dmm_msg(ctypes.c_void_p(a.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                       count, K, ws, T, _stream_handle(stream)))
+    return out
+
+
+def handshake(Fi, Fj, phiL, phiR, ws: int, T: int, stream=None):
+    """Device Handshake (Alg.5 P:811-830) on int32 CUDA tensors [count, K];
+    returns (phi_ij, phi_ji')."""
+    import torch
+    Fi, Fj, phiL, phiR = (t.contiguous() for t in (Fi, Fj, phiL, phiR))
+    oij = torch.empty_like(Fi)
+    oji = torch.empty_like(Fi)
+    count, K = Fi.shape
+    _prim_check(load_library().dmm_handshake(*(ctypes.c_void_p(t.data_ptr()) for t in (Fi, Fj, phiL, phiR, oij, oji)),
+                                             count, K, ws, T, _stream_handle(stream)))
+    return oij, oji
 
 
 class Context:
@@ -148,6 +181,10 @@ class Context:
     def set_profiling(self, enable: bool = True):
         """Record CUDA events around every kernel launch (on its stream)."""
         self._call("dmm_set_profiling", 1 if enable else 0)
+
+    def set_wave_bytes(self, nbytes: int):
+        """L2 wave budget of the chain-DP launches (0 = one launch per half-step)."""
+        self._call("dmm_set_tuning", TUNE_WAVE_BYTES, int(nbytes))
 
     def read_profile(self):
         """{class: (total_ms, launches)} since the last read (synchronises)."""

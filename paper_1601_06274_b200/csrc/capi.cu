@@ -23,6 +23,7 @@ struct dmm_ctx {
     std::string err;
     // event profiling (dmm_set_profiling)
     int profiling;
+    size_t wave_budget;   // bytes of chain data per launch wave (L2 sizing), 0 = one wave
     struct Rec { int cls; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
@@ -89,11 +90,12 @@ cudaEvent_t get_event(dmm_ctx* c) {
 // Brackets one kernel launch with events when profiling is on.
 struct Timed {
     dmm_ctx* c; int cls; cudaStream_t s; cudaEvent_t a = nullptr;
-    Timed(dmm_ctx* c_, int cls_, cudaStream_t s_) : c(c_), cls(cls_), s(s_) {
+    int count;
+    Timed(dmm_ctx* c_, int cls_, cudaStream_t s_, int count_ = 1) : c(c_), cls(cls_), s(s_), count(count_) {
         if (c->profiling) { a = get_event(c); cudaEventRecord(a, s); }
     }
     ~Timed() {
-        c->launches += 1;
+        c->launches += count;
         if (a) {
             cudaEvent_t b = get_event(c);
             cudaEventRecord(b, s);
@@ -155,6 +157,7 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->iters_done = new int[cfg->batch]();
     c->launches = 0;
     c->profiling = 0;
+    c->wave_budget = 0;
     if (cudaSetDevice(device) != cudaSuccess) {
         dmm_destroy(c);
         return DMM_E_CUDA;
@@ -213,11 +216,20 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
             a.fbits = ctx->cfg.frac_bits;
             a.ws = (v ? ctx->cfg.w_v : ctx->cfg.w_h) << ctx->cfg.frac_bits;
             a.wsT = a.ws * T;
+            a.T = T;
             a.first = (t == 0 && v == 0);
             a.last = (t == iterations - 1 && v == 1);
             a.bound_slot = 2 * t + v;
-            Timed tm(ctx, 2 + v, s);
-            dmm::launch_hm_pass(a, v, nframes, s);
+            // L2-sized waves: chain data (F records) of one wave fits the budget
+            const int chains = v ? ctx->L.W : ctx->L.H;
+            const size_t per_chain = (size_t)(v ? ctx->L.H : ctx->L.W) * ctx->KP * (v ? 4 : 5) * nframes;
+            int wave = 0;
+            if (ctx->wave_budget > 0) {
+                const size_t nw = (per_chain * chains + ctx->wave_budget - 1) / ctx->wave_budget;
+                if (nw > 1) wave = (int)((chains + nw - 1) / nw);
+            }
+            Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
+            dmm::launch_hm_pass(a, v, nframes, wave, s);
         }
     }
     {
@@ -319,6 +331,13 @@ dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const
 }
 
 int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value) {
+    if (!ctx) return DMM_E_ARG;
+    if (param == DMM_TUNE_WAVE_BYTES && value >= 0) { ctx->wave_budget = (size_t)value; return DMM_OK; }
+    ctx->err = "unknown tuning parameter";
+    return DMM_E_ARG;
+}
 
 dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable) {
     if (!ctx) return DMM_E_ARG;

@@ -67,6 +67,7 @@ struct PassArgs {
     int fbits;        // F
     int ws;           // w * 2^F
     int wsT;          // w * 2^F * T
+    int T;            // effective truncation min(T, K)
     int first;        // H pass of iteration 0: g_ == 0, not read
     int last;         // V pass of the last iteration: write labels
     int bound_slot;   // index into bounds[]
@@ -76,7 +77,11 @@ struct PassArgs {
 void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t pitch,
                    const uint8_t* left, const uint8_t* right, cudaStream_t s);
 void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s);
-void launch_hm_pass(const PassArgs& a, int vertical, int nframes, cudaStream_t s);
+// One H (vertical = 0) or V (vertical = 1) half-step over all chains, launched
+// in waves of `wave` chains (0 = all at once); returns nothing, launches
+// hm_launches_per_pass() kernels.
+void launch_hm_pass(const PassArgs& a, int vertical, int nframes, int wave, cudaStream_t s);
+int hm_launches_per_pass(const PassArgs& a, int vertical, int wave);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);

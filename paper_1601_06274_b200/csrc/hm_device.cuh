@@ -1,0 +1,184 @@
+// hm_device.cuh -- device primitives of the chain DP shared by the Dual MM
+// half-step kernels (hm.cu) and the primitive entry points (primitives.cu):
+// register-vector loads / stores, cp.async helpers and Msg (Eq. msg-pass
+// P:663-667; Msg of Alg.5).
+#pragma once
+#include <climits>
+
+#include "dmm_internal.cuh"
+
+namespace dmm {
+
+constexpr int kCMax = 12;    // longest leaf block (nodes)
+constexpr int kDepth = 4;    // pending right pieces in a leaf block (ceil(log2 kCMax))
+constexpr int kRing = 8;     // cp.async ring slots per warp
+
+// ------------------------------------------------------------ small helpers
+template <int LPL>
+__device__ __forceinline__ void ld_i32(const int32_t* p, int (&v)[LPL]) {
+    if constexpr (LPL == 1) {
+        v[0] = p[0];
+    } else if constexpr (LPL == 2) {
+        int2 t = *reinterpret_cast<const int2*>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < LPL / 4; ++q) {
+            int4 t = reinterpret_cast<const int4*>(p)[q];
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+    }
+}
+
+template <int LPL>
+__device__ __forceinline__ void st_i32(int32_t* p, const int (&v)[LPL]) {
+    if constexpr (LPL == 1) {
+        p[0] = v[0];
+    } else if constexpr (LPL == 2) {
+        *reinterpret_cast<int2*>(p) = make_int2(v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < LPL / 4; ++q)
+            reinterpret_cast<int4*>(p)[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+}
+
+template <int LPL>
+__device__ __forceinline__ void ld_u8(const uint8_t* p, int (&v)[LPL]) {
+    if constexpr (LPL == 1) {
+        v[0] = p[0];
+    } else if constexpr (LPL == 2) {
+        unsigned t = *reinterpret_cast<const unsigned short*>(p);
+        v[0] = t & 0xff; v[1] = t >> 8;
+    } else {
+#pragma unroll
+        for (int q = 0; q < LPL / 4; ++q) {
+            unsigned t = reinterpret_cast<const unsigned*>(p)[q];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) v[4 * q + b] = __byte_perm(t, 0, 0x4440 + b);
+        }
+    }
+}
+
+template <int LPL>
+__device__ __forceinline__ void st_u8(uint8_t* p, const int (&v)[LPL]) {
+    if constexpr (LPL == 1) {
+        p[0] = (uint8_t)v[0];
+    } else if constexpr (LPL == 2) {
+        *reinterpret_cast<unsigned short*>(p) = (unsigned short)((v[0] & 0xff) | (v[1] << 8));
+    } else {
+#pragma unroll
+        for (int q = 0; q < LPL / 4; ++q)
+            reinterpret_cast<unsigned*>(p)[q] =
+                __byte_perm(__byte_perm(v[4 * q], v[4 * q + 1], 0x0040), __byte_perm(v[4 * q + 2], v[4 * q + 3], 0x0040),
+                            0x5410);
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ------------------------------------------------------------------- Msg
+// Generic exact distance transform on a warp-held K-vector:
+//   MAX = false: x(b) := min_a x(a) + ws*min(|a-b|, T)      (Msg, min-plus)
+//   MAX = true:  x(b) := max_a x(a) - ws*min(|a-b|, T)      (= -Msg(-x))
+// The max-plus form computes the bounce-back Msg(-phi_ij) of Alg.5 without
+// negating first: ptxas 12.9 (sm_100a) folds the negations of a neg -> min
+// tree into VIMNMX3 and drops one of them (SASS VIMNMX3 R8, R15, R27, R8 with
+// R27 = +out1), which gave wrong phi_ji' for LPL >= 4.
+//  WIN: T <= LPL + 1, so every label within distance T-1 lies in this lane or
+//  a neighbouring one; candidates from lanes further away are beaten by the
+//  truncation term.  Lanes 0 / 31 have no left / right neighbour: the shuffle
+//  returns their own value, which must be masked (own fw[LPL-1] + ws*(e+1)
+//  would understate the distance to in-lane labels a > e when LPL >= 3).
+template <bool MAX>
+__device__ __forceinline__ int dt_op(int a, int b) { return MAX ? max(a, b) : min(a, b); }
+template <bool MAX>
+__device__ __forceinline__ int dt_addop(int a, int w, int c) {      // op(a + w, c), w signed
+    return MAX ? __viaddmax_s32(a, w, c) : __viaddmin_s32(a, w, c);
+}
+template <bool MAX>
+__device__ __forceinline__ int dt_op3(int a, int b, int c) {
+    return MAX ? __vimax3_s32(a, b, c) : __vimin3_s32(a, b, c);
+}
+
+template <int LPL, bool PAD, bool WIN, bool MAX = false>
+__device__ __forceinline__ void dtrans(int (&x)[LPL], int ws_, int wsT_, int lane, int K) {
+    const int big = MAX ? -kBig : kBig;
+    const int ws = MAX ? -ws_ : ws_;
+    const int wsT = MAX ? -wsT_ : wsT_;
+    if constexpr (PAD) {
+#pragma unroll
+        for (int e = 0; e < LPL; ++e)
+            if (lane * LPL + e >= K) x[e] = big;
+    }
+    int lred = x[0];
+#pragma unroll
+    for (int e = 1; e < LPL; ++e) lred = dt_op<MAX>(lred, x[e]);
+    const int cap = (MAX ? __reduce_max_sync(kFull, lred) : __reduce_min_sync(kFull, lred)) + wsT;
+    int fw[LPL], bw[LPL];
+    fw[0] = x[0];
+#pragma unroll
+    for (int e = 1; e < LPL; ++e) fw[e] = dt_addop<MAX>(fw[e - 1], ws, x[e]);
+    bw[LPL - 1] = x[LPL - 1];
+#pragma unroll
+    for (int e = LPL - 2; e >= 0; --e) bw[e] = dt_addop<MAX>(bw[e + 1], ws, x[e]);
+    int inf, inb;
+    if constexpr (WIN) {
+        inf = __shfl_up_sync(kFull, fw[LPL - 1], 1);
+        inb = __shfl_down_sync(kFull, bw[0], 1);
+    } else {
+        int cf = fw[LPL - 1], cb = bw[0];
+        const int step = ws * LPL;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int tf = __shfl_up_sync(kFull, cf, d);
+            const int tb = __shfl_down_sync(kFull, cb, d);
+            if (lane >= d) cf = dt_addop<MAX>(tf, step * d, cf);
+            if (lane + d < 32) cb = dt_addop<MAX>(tb, step * d, cb);
+        }
+        inf = __shfl_up_sync(kFull, cf, 1);
+        inb = __shfl_down_sync(kFull, cb, 1);
+    }
+    if (lane == 0) inf = big;
+    if (lane == 31) inb = big;
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) {
+        const int vf = dt_addop<MAX>(inf, ws * (e + 1), fw[e]);
+        const int vb = dt_addop<MAX>(inb, ws * (LPL - e), bw[e]);
+        x[e] = dt_op3<MAX>(vf, vb, cap);
+    }
+}
+
+// out(b) = min_a x(a) + ws*min(|a-b|, T), in place, exact (Msg).
+template <int LPL, bool PAD, bool WIN>
+__device__ __forceinline__ void msg(int (&x)[LPL], int ws, int wsT, int lane, int K) {
+    dtrans<LPL, PAD, WIN, false>(x, ws, wsT, lane, K);
+}
+
+// Handshake (Alg.5, readings R9/R10) on register vectors.
+// In: pl = message into i from the left, pr = message into j from the right,
+// Fi, Fj = node costs.  Out: pl = phi_ij (into j), pr = phi_ji' (into i).
+template <int LPL, bool PAD, bool WIN>
+__device__ __forceinline__ void handshake_regs(const int (&Fi)[LPL], const int (&Fj)[LPL], int (&pl)[LPL],
+                                               int (&pr)[LPL], int ws, int wsT, int lane, int K) {
+    int pji[LPL], t_[LPL];
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) pji[e] = Fj[e] + pr[e];
+    msg<LPL, PAD, WIN>(pji, ws, wsT, lane, K);               // phi_ji := Msg(f_j + phi_{j+1,j})
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) t_[e] = (pl[e] + Fi[e] - pji[e]) >> 1;   // floor(m_i/2 - phi_ji)
+    msg<LPL, PAD, WIN>(t_, ws, wsT, lane, K);                // phi_ij
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) pl[e] = t_[e];
+    dtrans<LPL, PAD, WIN, true>(t_, ws, wsT, lane, K);       // bounce back: Msg(-phi_ij) = -maxplus(phi_ij)
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) pr[e] = -t_[e];
+}
+
+}  // namespace dmm

@@ -160,3 +160,36 @@ def test_c2_full_size(orc):
     g = _run_gpu(left, right, *args)
     o = _run_oracle(orc, left, right, *args, nthreads=max(1, min(16, __import__("os").cpu_count() or 1)))
     _compare(g, o)
+
+
+# ---------------------------------------------------------------- primitives
+@pytest.mark.parametrize("K", [1, 5, 16, 31, 32, 33, 64, 100, 128, 129, 200, 256])
+def test_msg_primitive(orc, K):
+    """Device Msg vs the oracle's Msg, all code paths:
+    padding (K < 32*LPL), one-hop window (T <= LPL+1) and full scan."""
+    import paper_1601_06274_b200 as dmm
+    rng = np.random.default_rng(K)
+    for T in sorted({1, 2, 3, 4, 5, 8, 9, K, K + 3}):
+        for ws in (0, 1, 48, 4080):
+            a = rng.integers(-200000, 200000, size=(64, K))
+            g = dmm.msg(torch.from_numpy(a.astype(np.int32)).cuda(), ws, T).cpu().numpy()
+            o = np.stack([orc.msg(v, ws, T) for v in a])
+            assert np.array_equal(g.astype(np.int64), o), (K, T, ws)
+
+
+@pytest.mark.parametrize("K", [3, 32, 64, 128, 256])
+def test_handshake_primitive(orc, K):
+    """Device Handshake vs Alg.5 written with the oracle's
+    Msg (reading R9: floor halving)."""
+    import paper_1601_06274_b200 as dmm
+    rng = np.random.default_rng(100 + K)
+    for T in (1, 4, 7):
+        ws = 48
+        Fi, Fj, pL, pR = (rng.integers(-5000, 5000, size=(32, K)) for _ in range(4))
+        gij, gji = dmm.handshake(*(torch.from_numpy(x.astype(np.int32)).cuda() for x in (Fi, Fj, pL, pR)), ws, T)
+        for v in range(32):
+            pji = orc.msg(Fj[v] + pR[v], ws, T)
+            m = pL[v] + Fi[v] + pji
+            pij = orc.msg(np.floor_divide(m - 2 * pji, 2), ws, T)
+            pji2 = orc.msg(-pij, ws, T)
+            assert np.array_equal(gij[v].cpu().numpy(), pij) and np.array_equal(gji[v].cpu().numpy(), pji2)
