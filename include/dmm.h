@@ -26,7 +26,8 @@
  *    exported label-contiguous and dense: [H][W][K].
  *  - Errors: DMM_E_ARG invalid argument / config, DMM_E_SHAPE pitch < width,
  *    DMM_E_STATE solve before cost volume / result before solve,
- *    DMM_E_CUDA a CUDA runtime error (text in dmm_last_error()).
+ *    DMM_E_CUDA a CUDA runtime error (text in dmm_last_error()),
+ *    DMM_E_RANGE config outside the exact compact-storage range (dmm_create).
  */
 #ifndef DMM_B200_H
 #define DMM_B200_H
@@ -69,7 +70,12 @@ typedef struct dmm_ctx dmm_ctx;
 DMM_API size_t dmm_workspace_bytes(const dmm_config* cfg);
 
 /* Bind a context to caller-owned device memory `workspace` (>= the size above,
- * 256-byte aligned) on CUDA device `device`.  *out receives the context. */
+ * 256-byte aligned) on CUDA device `device`.  *out receives the context.
+ * The duals are stored as lossless u16-span records (DESIGN.md "Compact
+ * duals"); configurations whose proven span bound
+ *   (2 * max(w_h, w_v) * min(trunc, K-1) + max(census bits, oob)) * 2^frac_bits
+ * exceeds 65535 are rejected with DMM_E_RANGE (e.g. defaults w=3, T=4, F=4,
+ * 5x5 census: 768). */
 DMM_API dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int device,
                       dmm_ctx** out);
 DMM_API void dmm_destroy(dmm_ctx* ctx);
@@ -152,6 +158,9 @@ DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches)
  * re-reads across hierarchy levels stay in the 126 MB L2; 0 = one launch.
  * Default 0 (measured: waves cost more occupancy than they save in L2 misses). */
 #define DMM_TUNE_WAVE_BYTES 1
+/* Debug: value != 0 makes dmm_solve stop after the first H half-step (the
+ * bound history then holds only b_0; for parity taps of f_ after H_1). */
+#define DMM_TUNE_DEBUG_STOP_AFTER_H 2
 DMM_API dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value);
 
 DMM_API const char* dmm_status_str(dmm_status s);

@@ -17,7 +17,7 @@ import numpy as np
 __all__ = ["Context", "DmmError", "library_path", "load_library", "EXPORTS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_lib", "libdmm_b200.so")
+_LIB_PATH = os.environ.get("DMM_B200_LIB") or os.path.join(_HERE, "_lib", "libdmm_b200.so")
 _lib = None
 
 # every entry point declared in include/dmm.h

@@ -24,6 +24,7 @@ struct dmm_ctx {
     // event profiling (dmm_set_profiling)
     int profiling;
     size_t wave_budget;   // bytes of chain data per launch wave (L2 sizing), 0 = one wave
+    int stop_after_h;     // debug: dmm_solve runs only the first H half-step
     struct Rec { int cls; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
@@ -43,6 +44,20 @@ bool valid(const dmm_config* c) {
            c->batch >= 1 && c->max_iters >= 1 && c->max_iters <= 1024;
 }
 
+// Span bound of every stored K-vector: a Msg
+// output spans <= ws*min(T, K-1); f_ = L + D_s + R and D_s + g_ = D_s + L + R
+// span <= (2*w*min(T, K-1) + maxD) * 2^F.  Records store u16 offsets.
+long long span_bound(const dmm_config* c) {
+    const int K = c->d_max - c->d_min + 1;
+    const int r = c->census_radius;
+    const int bits = (2 * r + 1) * (2 * r + 1) - 1;
+    const int oob = c->oob_cost >= 0 ? c->oob_cost : bits / 2;
+    const long long maxD = oob > bits ? oob : bits;
+    const long long w = c->w_h > c->w_v ? c->w_h : c->w_v;
+    const long long T = c->trunc < K - 1 ? c->trunc : (K - 1);
+    return (2 * w * T + maxD) << c->frac_bits;
+}
+
 int kp_of(int K) {
     int lpl = 1;
     while (32 * lpl < K) lpl *= 2;
@@ -60,8 +75,8 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->codes_l = (uint32_t*)take(4 * px);
     off->codes_r = (uint32_t*)take(4 * px);
     off->D = (uint8_t*)take(cells);
-    off->fdual = (int32_t*)take(4 * cells);
-    off->gdual = (int32_t*)take(4 * cells);
+    off->fv = (uint8_t*)take(px * (size_t)dmm::rec_bytes((int)KP));
+    off->fh = (uint8_t*)take(px * (size_t)dmm::rec_bytes((int)KP));
     off->fwd = (int32_t*)take(4 * cells);
     off->bwd = (int32_t*)take(4 * cells);
     off->labels = (uint8_t*)take(px);
@@ -125,6 +140,7 @@ size_t dmm_workspace_bytes(const dmm_config* cfg) {
 dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int device,
                       dmm_ctx** out) {
     if (!out || !valid(cfg) || !workspace || ((uintptr_t)workspace & 255)) return DMM_E_ARG;
+    if (span_bound(cfg) > 65535) return DMM_E_RANGE;
     *out = nullptr;
     if (bytes < dmm_workspace_bytes(cfg)) return DMM_E_ARG;
     dmm_ctx* c = new (std::nothrow) dmm_ctx();
@@ -143,8 +159,8 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.codes_l = (uint32_t*)(b + (size_t)off.codes_l);
     c->L.base.codes_r = (uint32_t*)(b + (size_t)off.codes_r);
     c->L.base.D = (uint8_t*)(b + (size_t)off.D);
-    c->L.base.fdual = (int32_t*)(b + (size_t)off.fdual);
-    c->L.base.gdual = (int32_t*)(b + (size_t)off.gdual);
+    c->L.base.fv = (uint8_t*)(b + (size_t)off.fv);
+    c->L.base.fh = (uint8_t*)(b + (size_t)off.fh);
     c->L.base.fwd = (int32_t*)(b + (size_t)off.fwd);
     c->L.base.bwd = (int32_t*)(b + (size_t)off.bwd);
     c->L.base.labels = (uint8_t*)(b + (size_t)off.labels);
@@ -158,6 +174,7 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->launches = 0;
     c->profiling = 0;
     c->wave_budget = 0;
+    c->stop_after_h = 0;
     if (cudaSetDevice(device) != cudaSuccess) {
         dmm_destroy(c);
         return DMM_E_CUDA;
@@ -230,7 +247,9 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
             }
             Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
             dmm::launch_hm_pass(a, v, nframes, wave, s);
+            if (ctx->stop_after_h) break;
         }
+        if (ctx->stop_after_h) break;
     }
     {
         Timed tm(ctx, 4, s);
@@ -305,8 +324,8 @@ dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void*
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
     if (ctx->iters_done[frame] < 1) return DMM_E_STATE;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
-    dmm::launch_unpad_i32(which ? P.gdual : P.fdual, dst, (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP,
-                          (cudaStream_t)stream);
+    dmm::launch_decode_rec(which ? P.fh : P.fv, which ? P.D : nullptr, ctx->cfg.frac_bits, dst,
+                           (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
     return check_launch(ctx, "copy dual");
 }
 
@@ -335,6 +354,7 @@ int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
 dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value) {
     if (!ctx) return DMM_E_ARG;
     if (param == DMM_TUNE_WAVE_BYTES && value >= 0) { ctx->wave_budget = (size_t)value; return DMM_OK; }
+    if (param == DMM_TUNE_DEBUG_STOP_AFTER_H) { ctx->stop_after_h = value != 0; return DMM_OK; }
     ctx->err = "unknown tuning parameter";
     return DMM_E_ARG;
 }

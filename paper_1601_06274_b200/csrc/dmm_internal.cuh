@@ -4,13 +4,17 @@
 // HBM layout of one frame:
 //   codes  u32 [H][W]           census codes, left and right
 //   D      u8  [H][W][KP]       cost volume, label-contiguous, KP = 32*LPL >= K
-//   fdual  i32 [H][W][KP]       f_ (horizontal minorant), written by the H pass
-//   gdual  i32 [H][W][KP]       g_ (vertical minorant),   written by the V pass
+//   fv     rec [H][W]           f_ = minorant of the H pass (the V pass's unaries)
+//   fh     rec [H][W]           D*2^F + g_ (the H pass's unaries), g_ = minorant of the V pass
 //   fwd    i32 [H][W][KP]       message scratch: message into a node from the left / top
 //   bwd    i32 [H][W][KP]       message scratch: message into a node from the right / bottom
 //   labels u8  [H][W]
-// Both chain orientations read a node's K-vector as one contiguous KP-element
-// run, so H chains (stride KP) and V chains (stride W*KP) are both coalesced.
+// rec = compact lossless K-vector record of REC = 2*KP + 16 bytes:
+//   u16 v[KP] | int32 base | 12 B pad,  value(k) = base + v[k], base = min_k.
+// Lossless because every stored vector has a span (max - min over labels)
+// below 2^16 (checked at dmm_create).
+// Both chain orientations read a node's K-vector as one contiguous record,
+// so H chains (stride REC) and V chains (stride W*REC) are both coalesced.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -28,8 +32,8 @@ struct FramePtrs {
     uint32_t* codes_l;
     uint32_t* codes_r;
     uint8_t* D;
-    int32_t* fdual;
-    int32_t* gdual;
+    uint8_t* fv;
+    uint8_t* fh;
     int32_t* fwd;
     int32_t* bwd;
     uint8_t* labels;
@@ -44,6 +48,8 @@ struct Layout {
     int W, H, K, KP;
 };
 
+__host__ __device__ constexpr int rec_bytes(int KP) { return 2 * KP + 16; }
+
 __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     FramePtrs p = L.base;
     const size_t o = (size_t)f * L.frame_bytes;
@@ -51,8 +57,8 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.codes_l = (uint32_t*)((char*)p.codes_l + o);
     p.codes_r = (uint32_t*)((char*)p.codes_r + o);
     p.D += o;
-    p.fdual = (int32_t*)((char*)p.fdual + o);
-    p.gdual = (int32_t*)((char*)p.gdual + o);
+    p.fv += o;
+    p.fh += o;
     p.fwd = (int32_t*)((char*)p.fwd + o);
     p.bwd = (int32_t*)((char*)p.bwd + o);
     p.labels += o;
@@ -85,7 +91,9 @@ int hm_launches_per_pass(const PassArgs& a, int vertical, int wave);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
-void launch_unpad_i32(const int32_t* src, int32_t* dst, long long cells, int K, int KP,
-                      cudaStream_t s);
+// Expand compact records to dense int32 [cells][K]; if D != nullptr subtract
+// D*2^fbits (recovers g_ from fh).
+void launch_decode_rec(const uint8_t* rec, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K,
+                       int KP, cudaStream_t s);
 
 }  // namespace dmm

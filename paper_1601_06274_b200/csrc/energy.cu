@@ -49,9 +49,24 @@ __global__ void unpad_kernel(const T* __restrict__ src, T* __restrict__ dst, lon
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s) {
     unpad_kernel<uint8_t><<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
 }
-void launch_unpad_i32(const int32_t* src, int32_t* dst, long long cells, int K, int KP,
-                      cudaStream_t s) {
-    unpad_kernel<int32_t><<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
+__global__ void decode_rec_kernel(const uint8_t* __restrict__ rec, const uint8_t* __restrict__ D, int fbits,
+                                  int32_t* __restrict__ dst, long long cells, int K, int KP) {
+    const int R = rec_bytes(KP);
+    const long long n = cells * K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / K;
+        const int k = (int)(i - c * K);
+        const uint8_t* r = rec + c * R;
+        int v = *reinterpret_cast<const int32_t*>(r + 2 * KP) + reinterpret_cast<const uint16_t*>(r)[k];
+        if (D) v -= (int)D[c * KP + k] << fbits;
+        dst[i] = v;
+    }
+}
+
+void launch_decode_rec(const uint8_t* rec, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K,
+                       int KP, cudaStream_t s) {
+    decode_rec_kernel<<<4 * 148, 256, 0, s>>>(rec, D, fbits, dst, cells, K, KP);
 }
 
 }  // namespace dmm

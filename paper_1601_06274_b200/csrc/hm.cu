@@ -4,47 +4,52 @@
 //
 // Mapping:
 //  * one CTA per chain, NW warps; a warp owns one K-vector at a time with the
-//    label dimension in registers, LPL = KP/32 consecutive labels per lane.
-//  * Msg (Eq. msg-pass, Msg of Alg.5) for
-//    f_ij = ws*min(|a-b|, T) is computed exactly: in-lane forward/backward
-//    envelopes, a one-hop neighbour exchange (2 shuffles) when T <= LPL + 1 or a
-//    Kogge-Stone min-plus scan otherwise, and the truncation cap
-//    min(a) + ws*T from one redux.sync.min.
-//  * "global levels" (subchains longer than kCMax): processed breadth first,
-//    one warp per subchain; only the message direction whose boundary changed
-//    is recomputed (Fig.11's dots are reused: the "spine" messages a later level
-//    needs are kept in the fwd/bwd scratch arrays, L2-resident).  Node data
-//    F = D*2^F + g_ (H) or f_ (V) streams through a per-warp cp.async ring of
-//    kRing slots whose producer runs ahead across level barriers (the data
-//    does not depend on the messages).
-//  * "leaf blocks" (the 2^l* subchains of length <= kCMax): one warp stages the
-//    block's F in shared memory and finishes its whole sub-hierarchy on chip,
-//    depth first, with the forward and backward passes of each piece
-//    interleaved (two independent Msg chains -> ILP).  Leaves [p,p] with
-//    boundary messages L, R give lambda = L + F + R (reading R8):
-//    H writes f_ = lambda - g_ = L + D*2^F + R, V writes g_ = lambda - f_ = L + R;
-//    the node minima sum to the dual bound (exactness) and the last V pass
+//    label dimension in registers, LPL = KP/32 consecutive labels per lane;
+//    Msg / Handshake are the register-level primitives of hm_device.cuh.
+//  * node data F (the pass's unaries: D*2^F + g_ for H, f_ for V) are compact
+//    u16-span records (dmm_internal.cuh); they stream into a per-warp ring of
+//    kNSlot chunks x kCH nodes filled by TMA bulk copies (cp.async.bulk, one
+//    lane per node, one mbarrier per chunk).  The producer walks the warp's
+//    whole consumption order (RunSeq) and runs ahead across level barriers:
+//    node data never depend on the messages.
+//  * "global levels" (subchains longer than kCMax): breadth first, one warp
+//    per subchain; only the message direction whose boundary changed is
+//    recomputed (Fig.11's dots are reused: "spine" messages a later level needs
+//    are kept in the fwd/bwd scratch arrays, L2-resident); each task's two
+//    message loads are issued one task ahead.
+//  * "leaf blocks" (the 2^l* subchains of length <= kCMax): one warp copies
+//    the block's F (decoded to int32) and D rows into shared memory and
+//    finishes the sub-hierarchy on chip, depth first, the forward and backward
+//    passes of each piece interleaved (two independent Msg chains -> ILP).
+//    A leaf [p,p] with boundary messages L, R has lambda = L + F + R (reading
+//    R8); the pass writes L + R + D*2^F, which is f_ = lambda - g_ for H and
+//    D*2^F + g_ (the next H pass's unaries) for V, as a compact record.  Node
+//    minima of lambda sum to the dual bound (exactness); the last V pass
 //    writes the lowest-index argmin as the label (R13, R14).
-//  * chains are launched in L2-sized waves (host side) so the global levels'
-//    re-reads of F hit the 126 MB L2.
 // All arithmetic is exact int32 (ranges in DESIGN.md): bit-identical to the
 // CPU oracle whatever the evaluation order.
 #include "hm_device.cuh"
 
 namespace dmm {
 
-// ------------------------------------------------------------ the kernel
+constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
+constexpr int kDepth = 4;    // pending right pieces in a leaf block (ceil(log2 kCMax))
+constexpr int kCH = 4;       // nodes per ring chunk
+constexpr int kNSlot = 4;    // ring chunks per warp (prefetch depth kNSlot * kCH nodes)
+
+__host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
 struct HmShared {   // per-warp shared memory carve-up (bytes)
-    int ring, leafF, leafD, stack, stackIdx, total;
-    __host__ __device__ HmShared(int KP, bool vert) {
-        const int rec = vert ? KP * 4 : KP * 5;
+    int rec, slot, ring, mbar, leafF, leafD, stack, total;
+    __host__ __device__ HmShared(int KP) {
+        rec = rec_bytes(KP);
+        slot = kCH * (rec + KP);               // kCH F records, then kCH D rows
         ring = 0;
-        leafF = ring + kRing * rec;
+        mbar = align_up(ring + kNSlot * slot, 8);
+        leafF = align_up(mbar + kNSlot * 8, 16);
         leafD = leafF + kCMax * KP * 4;
-        stack = leafD + (vert ? 0 : kCMax * KP);
-        stackIdx = stack + kDepth * 2 * KP * 4;
-        total = stackIdx + kDepth * 8;
-        total = (total + 127) & ~127;
+        stack = leafD + kCMax * KP;
+        total = align_up(stack + kDepth * 2 * KP * 4, 128);
     }
 };
 
@@ -57,119 +62,141 @@ __device__ __forceinline__ void task_bounds(int n, int lev, int s, int& lo, int&
     }
 }
 
-// Producer side of the ring: enumerates, in consumption order, the nodes whose
-// F this warp will read (global-level passes, Handshake nodes j then i, then
-// the leaf blocks' nodes in ascending order).
-struct NodeSeq {
-    int n, lstar, warp, nw;
-    int lev, s, p, step, left, hs, hj, hi_;
+// The warp's node consumption order as runs of consecutive nodes: per global
+// task its pass (forward lo..i-1 or backward hi..j+1) then the Handshake pair
+// j, i; per leaf block lo..hi (these runs also carry the D rows).
+struct RunSeq {
+    int n, lstar, warp, nw, lev, s, phase;
     bool done;
-    __device__ __forceinline__ void start() {
-        while (true) {
-            if (lev > lstar) { done = true; return; }
-            if (lev == 0 && lstar > 0) {
-                if (s <= 1) {
-                    const int i = n / 2 - 1, j = i + 1;
-                    if (s == 0) { p = 0; step = 1; left = i; hs = 2; hj = j; hi_ = i; }
-                    else { p = n - 1; step = -1; left = n - 1 - j; hs = 0; }
-                    return;
-                }
-            } else if (s < (1 << lev)) {
-                int lo, hi;
-                task_bounds(n, lev, s, lo, hi);
-                if (lev == lstar) { p = lo; step = 1; left = hi - lo + 1; hs = 0; return; }
-                const int i = lo + (hi - lo + 1) / 2 - 1, j = i + 1;
-                if (!(s & 1)) { p = hi; step = -1; left = hi - j; }
-                else { p = lo; step = 1; left = i - lo; }
-                hs = 2; hj = j; hi_ = i;
-                return;
-            }
-            ++lev; s = warp;
-        }
-    }
     __device__ __forceinline__ void init(int n_, int lstar_, int warp_, int nw_) {
-        n = n_; lstar = lstar_; warp = warp_; nw = nw_; lev = 0; s = warp_; done = false;
-        start();
+        n = n_; lstar = lstar_; warp = warp_; nw = nw_; lev = 0; s = warp_; phase = 0; done = false;
     }
-    __device__ __forceinline__ bool next(int& node) {
+    // next non-empty run; false when exhausted
+    __device__ __forceinline__ bool next(int& start, int& dir, int& count, bool& leaf) {
         while (!done) {
-            if (left > 0) { node = p; p += step; --left; return true; }
-            if (hs == 2) { node = hj; hs = 1; return true; }
-            if (hs == 1) { node = hi_; hs = 0; return true; }
-            s += nw;
-            start();
+            if (lev > lstar) { done = true; break; }
+            leaf = false;
+            if (lev == 0 && lstar > 0) {
+                if (s > 1) { ++lev; s = warp; phase = 0; continue; }
+                const int i = n / 2 - 1, j = i + 1;
+                if (s == 0) {
+                    if (phase == 0) { phase = 1; start = 0; dir = 1; count = i; if (count > 0) return true; continue; }
+                    phase = 0; s += nw; start = j; dir = -1; count = 2; return true;
+                }
+                phase = 0; s += nw; start = n - 1; dir = -1; count = n - 1 - j;
+                if (count > 0) return true;
+                continue;
+            }
+            if (s >= (1 << lev)) { ++lev; s = warp; phase = 0; continue; }
+            int lo, hi;
+            task_bounds(n, lev, s, lo, hi);
+            if (lev == lstar) { s += nw; start = lo; dir = 1; count = hi - lo + 1; leaf = true; return true; }
+            const int i = lo + (hi - lo + 1) / 2 - 1, j = i + 1;
+            if (phase == 0) {
+                phase = 1;
+                if (!(s & 1)) { start = hi; dir = -1; count = hi - j; }
+                else { start = lo; dir = 1; count = i - lo; }
+                if (count > 0) return true;
+                continue;
+            }
+            phase = 0; s += nw; start = j; dir = -1; count = 2; return true;
         }
         return false;
     }
 };
 
-template <int LPL, bool VERT, bool PAD, bool WIN>
+template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
 struct Hm {
     static constexpr int KP = 32 * LPL;
+    static constexpr int REC = rec_bytes(KP);
+    static constexpr int SREC = FIRST ? KP : REC;   // bytes of a source record (FIRST: the D row)
     FramePtrs P;
+    const uint8_t* src;     // source records: FIRST ? D : (VERT ? fv : fh)
+    uint8_t* dst;           // output records: VERT ? fh : fv
     int W, K, c, lane, n;
     int fbits, ws, wsT;
-    bool first, last;
-    char* ring;
-    int rec;
-    NodeSeq seq;
-    int t, issued;
+    bool last;
     long long bsum;
+    // ring
+    uint8_t* ring;
+    uint64_t* mbar;
+    unsigned clen;                  // chunk length of slot s in bits 8s..8s+7 (per-lane copy:
+                                    // every lane runs the producer logic; no shared state)
+    int slotB;
+    RunSeq seq;
+    int r_start, r_dir, r_left;     // producer: rest of the current run
+    bool r_leaf;
+    int cslot, cidx, ccount;        // consumer position
+    unsigned cphase;                // consumer parity bit per slot
+    bool cwait;
 
-    __device__ __forceinline__ size_t q_of(int p) const {
-        return VERT ? (size_t)p * W + c : (size_t)c * W + p;
-    }
-    __device__ __forceinline__ size_t off(int p) const { return q_of(p) * KP + lane * LPL; }
+    __device__ __forceinline__ int q_of(int p) const { return VERT ? p * W + c : c * W + p; }
+    __device__ __forceinline__ size_t moff(int p) const { return (size_t)q_of(p) * KP + lane * LPL; }
     __device__ __forceinline__ void msg_(int (&x)[LPL]) const { msg<LPL, PAD, WIN>(x, ws, wsT, lane, K); }
 
-    // ---- ring
-    __device__ __forceinline__ void issue() {
-        int node;
-        if (seq.next(node)) {
-            char* slot = ring + (issued % kRing) * rec;
-            const size_t q = q_of(node);
-            if constexpr (VERT) {
-                const char* src = reinterpret_cast<const char*>(P.fdual + q * KP);
-#pragma unroll
-                for (int ch = lane; ch < KP / 4; ch += 32) cp_async16(slot + 16 * ch, src + 16 * ch);
-            } else {
-                if (!first) {
-                    const char* src = reinterpret_cast<const char*>(P.gdual + q * KP);
-#pragma unroll
-                    for (int ch = lane; ch < KP / 4; ch += 32) cp_async16(slot + 16 * ch, src + 16 * ch);
-                }
-                const char* srcd = reinterpret_cast<const char*>(P.D + q * KP);
-                if (lane < KP / 16) cp_async16(slot + KP * 4 + 16 * lane, srcd + 16 * lane);
-            }
+    // ---- producer: fill `slot` with the next chunk (<= kCH nodes of one run)
+    __device__ __forceinline__ void fill(int slot) {
+        while (r_left == 0) {
+            if (!seq.next(r_start, r_dir, r_left, r_leaf)) return;
         }
-        cp_async_commit();
-        ++issued;
+        const int cnt = r_left < kCH ? r_left : kCH;
+        uint8_t* sbase = ring + slot * slotB;
+        clen = (clen & ~(0xffu << (8 * slot))) | ((unsigned)cnt << (8 * slot));
+        if (lane == 0) mbar_expect_tx(&mbar[slot], (unsigned)(cnt * (SREC + (r_leaf && !FIRST ? KP : 0))));
+        __syncwarp();
+        // every lane read this slot through the generic proxy: order those reads
+        // before the async-proxy (TMA) overwrite
+        fence_proxy_async();
+        __syncwarp();
+        if (lane < cnt) {
+            const int node = r_start + r_dir * lane;
+            const size_t q = (size_t)q_of(node);
+            tma_load(sbase + lane * REC, src + q * SREC, SREC, &mbar[slot]);
+            if (!FIRST && r_leaf) tma_load(sbase + kCH * REC + lane * KP, P.D + q * KP, KP, &mbar[slot]);
+        }
+        r_start += r_dir * cnt;
+        r_left -= cnt;
     }
-    __device__ __forceinline__ void prologue() {
-#pragma unroll 1
-        for (int k = 0; k < kRing - 1; ++k) issue();
+    __device__ __forceinline__ void ring_init(char* wsm, const HmShared& lay) {
+        ring = reinterpret_cast<uint8_t*>(wsm + lay.ring);
+        mbar = reinterpret_cast<uint64_t*>(wsm + lay.mbar);
+        slotB = lay.slot;
+        if (lane == 0) {
+            for (int k = 0; k < kNSlot; ++k) mbar_init(&mbar[k], 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+        r_left = 0;
+        clen = 0;
+        cslot = 0; cidx = 0; ccount = 0; cphase = 0; cwait = true;
+        for (int k = 0; k < kNSlot; ++k) fill(k);
     }
-    // Next F (and D for H) in consumption order.
+    // ---- consumer: next node's F (decoded) and, for leaf runs, its D row
+    template <bool WANT_D>
     __device__ __forceinline__ void pop(int (&F)[LPL], int (&Dv)[LPL]) {
-        issue();
-        cp_async_wait<kRing - 1>();
-        __syncwarp();
-        const char* slot = ring + (t % kRing) * rec;
-        ++t;
-        if constexpr (VERT) {
-            ld_i32<LPL>(reinterpret_cast<const int32_t*>(slot) + lane * LPL, F);
-        } else {
-            ld_u8<LPL>(reinterpret_cast<const uint8_t*>(slot + KP * 4) + lane * LPL, Dv);
-            if (!first) {
-                ld_i32<LPL>(reinterpret_cast<const int32_t*>(slot) + lane * LPL, F);
-#pragma unroll
-                for (int e = 0; e < LPL; ++e) F[e] += Dv[e] << fbits;
-            } else {
-#pragma unroll
-                for (int e = 0; e < LPL; ++e) F[e] = Dv[e] << fbits;
-            }
+        if (cwait) {
+            mbar_wait(&mbar[cslot], (cphase >> cslot) & 1u);
+            __syncwarp();     // the whole warp has observed the phase before any lane reads or refills
+            cphase ^= 1u << cslot;
+            ccount = (int)((clen >> (8 * cslot)) & 0xffu);
+            cidx = 0;
+            cwait = false;
         }
-        __syncwarp();
+        const uint8_t* sb = ring + cslot * slotB;
+        if constexpr (FIRST) {
+            ld_u8<LPL>(sb + cidx * REC + lane * LPL, Dv);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) F[e] = Dv[e] << fbits;
+        } else {
+            ld_rec<LPL>(sb + cidx * REC, lane, F);
+            if constexpr (WANT_D) ld_u8<LPL>(sb + kCH * REC + cidx * KP + lane * LPL, Dv);
+        }
+        if (++cidx == ccount) {
+            __syncwarp();
+            fill(cslot);
+            cslot = cslot + 1 == kNSlot ? 0 : cslot + 1;
+            cwait = true;
+        }
     }
 
     // ---- global-level passes (messages in the fwd/bwd scratch arrays)
@@ -181,12 +208,12 @@ struct Hm {
 #pragma unroll 1
         for (int p = lo; p < end; ++p) {
             int F[LPL], Dv[LPL];
-            pop(F, Dv);
+            pop<false>(F, Dv);
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi[e] += F[e];
             msg_(phi);
             if (p + 2 - lo == target) {
-                st_i32<LPL>(P.fwd + off(p + 1), phi);
+                st_i32<LPL>(P.fwd + moff(p + 1), phi);
                 --kk;
                 target = kk >= 0 ? (len0 >> kk) : INT_MAX;
             }
@@ -200,31 +227,26 @@ struct Hm {
 #pragma unroll 1
         for (int p = hi; p > end; --p) {
             int F[LPL], Dv[LPL];
-            pop(F, Dv);
+            pop<false>(F, Dv);
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi[e] += F[e];
             msg_(phi);
             if (hi - p + 2 == target) {
-                st_i32<LPL>(P.bwd + off(p - 1), phi);
+                st_i32<LPL>(P.bwd + moff(p - 1), phi);
                 --kk;
                 target = kk >= 0 ? (((lenB - 1) >> kk) + 1) : INT_MAX;
             }
         }
     }
-    // Handshake (Alg.5, R9/R10); Fj, Fi popped in that order.  On exit pl =
-    // phi_ij (left boundary of the right piece), pr = phi_ji' (right boundary
-    // of the left piece).
-    __device__ __forceinline__ void handshake(const int (&Fi)[LPL], const int (&Fj)[LPL], int (&pl)[LPL],
-                                              int (&pr)[LPL]) {
-        handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, ws, wsT, lane, K);
-    }
+    // Handshake (Alg.5); the ring delivers F_j then F_i.  Writes the
+    // children's new boundaries: fwd[j] = phi_ij, bwd[i] = phi_ji'.
     __device__ __forceinline__ void global_handshake(int i, int (&pl)[LPL], int (&pr)[LPL]) {
         int Fi[LPL], Fj[LPL], Dv[LPL];
-        pop(Fj, Dv);
-        pop(Fi, Dv);
-        handshake(Fi, Fj, pl, pr);
-        st_i32<LPL>(P.fwd + off(i + 1), pl);
-        st_i32<LPL>(P.bwd + off(i), pr);
+        pop<false>(Fj, Dv);
+        pop<false>(Fi, Dv);
+        handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, ws, wsT, lane, K);
+        st_i32<LPL>(P.fwd + moff(i + 1), pl);
+        st_i32<LPL>(P.bwd + moff(i), pr);
     }
 
     // ---- leaves
@@ -235,12 +257,12 @@ struct Hm {
 #pragma unroll
         for (int e = 0; e < LPL; ++e) {
             const int lr = L[e] + R[e];
-            o[e] = VERT ? lr : lr + (Dv[e] << fbits);
+            o[e] = lr + (Dv[e] << fbits);
             lam[e] = lr + F[e];
-            if (PAD && lane * LPL + e >= K) { o[e] = 0; lam[e] = INT_MAX; }
+            if (PAD && lane * LPL + e >= K) lam[e] = INT_MAX;
             lmin = min(lmin, lam[e]);
         }
-        st_i32<LPL>((VERT ? P.gdual : P.fdual) + off(node), o);
+        st_rec<LPL, PAD>(dst + (size_t)q_of(node) * REC, lane, o, K);
         const int gmin = __reduce_min_sync(kFull, lmin);
         bsum += gmin;
         if (VERT && last) {
@@ -256,27 +278,32 @@ struct Hm {
     // Whole sub-hierarchy of the block [lo0, lo0+m-1] on chip (depth first; the
     // pieces' forward / backward passes recompute both directions).
     __device__ __forceinline__ void leaf_block(int lo0, int m, int (&L)[LPL], int (&R)[LPL], int32_t* sF,
-                                               uint8_t* sD, int32_t* stk, int* stkIdx) {
+                                               uint8_t* sD, int32_t* stk) {
 #pragma unroll 1
         for (int k = 0; k < m; ++k) {
             int F[LPL], Dv[LPL];
-            pop(F, Dv);
+            pop<true>(F, Dv);
             st_i32<LPL>(sF + k * KP + lane * LPL, F);
-            if constexpr (!VERT) st_u8<LPL>(sD + k * KP + lane * LPL, Dv);
+            st_u8<LPL>(sD + k * KP + lane * LPL, Dv);
         }
-        __syncwarp();
         int lo = 0, hi = m - 1, sp = 0;
+        unsigned stkJ = 0;
 #pragma unroll 1
         while (true) {
             if (lo == hi) {
                 int F[LPL], Dv[LPL];
                 ld_i32<LPL>(sF + lo * KP + lane * LPL, F);
-                if constexpr (!VERT) ld_u8<LPL>(sD + lo * KP + lane * LPL, Dv);
+                ld_u8<LPL>(sD + lo * KP + lane * LPL, Dv);
                 emit(lo0 + lo, L, F, Dv, R);
                 if (sp == 0) break;
                 --sp;
                 __syncwarp();
-                lo = stkIdx[2 * sp]; hi = stkIdx[2 * sp + 1];
+                // pending piece k = [j_k, hi_k] with hi_0 = m-1 and
+                // hi_k = j_{k-1} - 1: only the j's are kept, 4 bits each, in a
+                // per-lane register (no lane reads shared state another lane
+                // may be rewriting)
+                lo = (int)((stkJ >> (4 * sp)) & 0xfu);
+                hi = sp == 0 ? m - 1 : (int)((stkJ >> (4 * (sp - 1))) & 0xfu) - 1;
                 ld_i32<LPL>(stk + (2 * sp) * KP + lane * LPL, L);
                 ld_i32<LPL>(stk + (2 * sp + 1) * KP + lane * LPL, R);
                 continue;
@@ -306,9 +333,9 @@ struct Hm {
             int Fi[LPL], Fj[LPL];
             ld_i32<LPL>(sF + i * KP + lane * LPL, Fi);
             ld_i32<LPL>(sF + j * KP + lane * LPL, Fj);
-            handshake(Fi, Fj, pl, pr);
+            handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, ws, wsT, lane, K);
             // push the right piece (j, hi, phi_ij, R); continue with (lo, i, L, phi_ji')
-            if (lane == 0) { stkIdx[2 * sp] = j; stkIdx[2 * sp + 1] = hi; }
+            stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
             st_i32<LPL>(stk + (2 * sp) * KP + lane * LPL, pl);
             st_i32<LPL>(stk + (2 * sp + 1) * KP + lane * LPL, R);
             ++sp;
@@ -319,31 +346,30 @@ struct Hm {
     }
 };
 
-template <int LPL, bool VERT, bool PAD, bool WIN, int NW>
+template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST, int NW>
 __global__ void __launch_bounds__(NW * 32) hm_kernel(PassArgs a, int chain0, int lstar) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
-    const HmShared lay(KP, VERT);
+    const HmShared lay(KP);
     char* wsm = smem + warp * lay.total;
 
-    Hm<LPL, VERT, PAD, WIN> h;
+    Hm<LPL, VERT, PAD, WIN, FIRST> h;
     h.P = frame_ptrs(a.L, a.frame0 + blockIdx.y);
+    h.src = FIRST ? h.P.D : (VERT ? h.P.fv : h.P.fh);
+    h.dst = VERT ? h.P.fh : h.P.fv;
     h.W = a.L.W; h.K = a.L.K; h.c = chain0 + blockIdx.x; h.lane = lane;
     h.n = VERT ? a.L.H : a.L.W;
     h.fbits = a.fbits; h.ws = a.ws; h.wsT = a.wsT;
-    h.first = a.first != 0; h.last = a.last != 0;
-    h.ring = wsm + lay.ring;
-    h.rec = VERT ? KP * 4 : KP * 5;
-    h.t = 0; h.issued = 0; h.bsum = 0;
+    h.last = a.last != 0;
+    h.bsum = 0;
     const int n = h.n;
     h.seq.init(n, lstar, warp, NW);
-    h.prologue();
+    h.ring_init(wsm, lay);
 
     int32_t* sF = reinterpret_cast<int32_t*>(wsm + lay.leafF);
     uint8_t* sD = reinterpret_cast<uint8_t*>(wsm + lay.leafD);
     int32_t* stk = reinterpret_cast<int32_t*>(wsm + lay.stack);
-    int* stkIdx = reinterpret_cast<int*>(wsm + lay.stackIdx);
     int zero[LPL];
 #pragma unroll
     for (int e = 0; e < LPL; ++e) zero[e] = 0;
@@ -354,47 +380,61 @@ __global__ void __launch_bounds__(NW * 32) hm_kernel(PassArgs a, int chain0, int
         int pl[LPL], pr[LPL];
 #pragma unroll
         for (int e = 0; e < LPL; ++e) { pl[e] = 0; pr[e] = 0; }
-        if (warp == 0) { st_i32<LPL>(h.P.fwd + h.off(0), zero); h.pass_fwd(0, i, pl); }
-        if (warp == 1) { st_i32<LPL>(h.P.bwd + h.off(n - 1), zero); h.pass_bwd(n - 1, i + 1, pr); st_i32<LPL>(h.P.bwd + h.off(i + 1), pr); }
+        if (warp == 0) { st_i32<LPL>(h.P.fwd + h.moff(0), zero); h.pass_fwd(0, i, pl); }
+        if (warp == 1) {
+            st_i32<LPL>(h.P.bwd + h.moff(n - 1), zero);
+            h.pass_bwd(n - 1, i + 1, pr);
+            st_i32<LPL>(h.P.bwd + h.moff(i + 1), pr);
+        }
         __syncthreads();
         if (warp == 0) {
-            ld_i32<LPL>(h.P.bwd + h.off(i + 1), pr);
+            ld_i32<LPL>(h.P.bwd + h.moff(i + 1), pr);
             h.global_handshake(i, pl, pr);
         }
         __syncthreads();
-        // ---- global levels 1 .. lstar-1
+        // ---- global levels 1 .. lstar-1; message loads issued one task ahead
 #pragma unroll 1
         for (int lev = 1; lev < lstar; ++lev) {
+            int nb_[LPL], ns_[LPL];    // next task's boundary and spine messages
+            auto load_msgs = [&](int s, int (&bnd)[LPL], int (&spn)[LPL]) {
+                int lo, hi;
+                task_bounds(n, lev, s, lo, hi);
+                const int ii = lo + (hi - lo + 1) / 2 - 1;
+                if (!(s & 1)) { ld_i32<LPL>(h.P.bwd + h.moff(hi), bnd); ld_i32<LPL>(h.P.fwd + h.moff(ii), spn); }
+                else { ld_i32<LPL>(h.P.fwd + h.moff(lo), bnd); ld_i32<LPL>(h.P.bwd + h.moff(ii + 1), spn); }
+            };
+            if (warp < (1 << lev)) load_msgs(warp, nb_, ns_);
 #pragma unroll 1
             for (int s = warp; s < (1 << lev); s += NW) {
+                int bnd[LPL], spn[LPL];
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) { bnd[e] = nb_[e]; spn[e] = ns_[e]; }
+                if (s + NW < (1 << lev)) load_msgs(s + NW, nb_, ns_);
                 int lo, hi;
                 task_bounds(n, lev, s, lo, hi);
                 const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
                 if (!(s & 1)) {   // left piece: left boundary kept -> reuse fwd, recompute bwd
-                    ld_i32<LPL>(h.P.bwd + h.off(hi), pr);
-                    ld_i32<LPL>(h.P.fwd + h.off(ii), pl);
-                    h.pass_bwd(hi, j, pr);
+                    h.pass_bwd(hi, j, bnd);
+                    h.global_handshake(ii, spn, bnd);
                 } else {          // right piece: right boundary kept -> reuse bwd, recompute fwd
-                    ld_i32<LPL>(h.P.fwd + h.off(lo), pl);
-                    ld_i32<LPL>(h.P.bwd + h.off(j), pr);
-                    h.pass_fwd(lo, ii, pl);
+                    h.pass_fwd(lo, ii, bnd);
+                    h.global_handshake(ii, bnd, spn);
                 }
-                h.global_handshake(ii, pl, pr);
             }
             __syncthreads();
         }
     } else {
-        if (warp == 0) { st_i32<LPL>(h.P.fwd + h.off(0), zero); st_i32<LPL>(h.P.bwd + h.off(n - 1), zero); }
+        if (warp == 0) { st_i32<LPL>(h.P.fwd + h.moff(0), zero); st_i32<LPL>(h.P.bwd + h.moff(n - 1), zero); }
         __syncthreads();
     }
-    // ---- leaf blocks at level lstar
+    // ---- leaf blocks at level lstar (boundary messages loaded one block ahead)
     const int nb = 1 << lstar;
     int L[LPL], R[LPL];
     if (warp < nb) {
         int lo, hi;
         task_bounds(n, lstar, warp, lo, hi);
-        ld_i32<LPL>(h.P.fwd + h.off(lo), L);
-        ld_i32<LPL>(h.P.bwd + h.off(hi), R);
+        ld_i32<LPL>(h.P.fwd + h.moff(lo), L);
+        ld_i32<LPL>(h.P.bwd + h.moff(hi), R);
     }
 #pragma unroll 1
     for (int s = warp; s < nb; s += NW) {
@@ -402,19 +442,18 @@ __global__ void __launch_bounds__(NW * 32) hm_kernel(PassArgs a, int chain0, int
         task_bounds(n, lstar, s, lo, hi);
         int L2[LPL], R2[LPL];
         const int s2 = s + NW;
-        if (s2 < nb) {      // prefetch the next block's boundary messages
+        if (s2 < nb) {
             int lo2, hi2;
             task_bounds(n, lstar, s2, lo2, hi2);
-            ld_i32<LPL>(h.P.fwd + h.off(lo2), L2);
-            ld_i32<LPL>(h.P.bwd + h.off(hi2), R2);
+            ld_i32<LPL>(h.P.fwd + h.moff(lo2), L2);
+            ld_i32<LPL>(h.P.bwd + h.moff(hi2), R2);
         }
-        h.leaf_block(lo, hi - lo + 1, L, R, sF, sD, stk, stkIdx);
+        h.leaf_block(lo, hi - lo + 1, L, R, sF, sD, stk);
         if (s2 < nb) {
 #pragma unroll
             for (int e = 0; e < LPL; ++e) { L[e] = L2[e]; R[e] = R2[e]; }
         }
     }
-    cp_async_wait<0>();
     if (lane == 0 && h.bsum != 0)
         atomicAdd(reinterpret_cast<unsigned long long*>(&h.P.bounds[a.bound_slot]),
                   (unsigned long long)h.bsum);
@@ -427,16 +466,16 @@ static int leaf_level(int n) {
     return l;
 }
 
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, bool WIN, bool FIRST>
 static void launch_cfg(const PassArgs& a, int vertical, int nframes, int wave_chains, cudaStream_t s) {
     constexpr int NW = 4;
     constexpr int KP = 32 * LPL;
     const int chains = vertical ? a.L.W : a.L.H;
     const int n = vertical ? a.L.H : a.L.W;
     const int lstar = leaf_level(n);
-    const HmShared lay(KP, vertical != 0);
+    const HmShared lay(KP);
     const int smem = NW * lay.total;
-    auto kern = vertical ? hm_kernel<LPL, true, PAD, WIN, NW> : hm_kernel<LPL, false, PAD, WIN, NW>;
+    auto kern = vertical ? hm_kernel<LPL, true, PAD, WIN, false, NW> : hm_kernel<LPL, false, PAD, WIN, FIRST, NW>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int wave = wave_chains > 0 ? wave_chains : chains;
     for (int c0 = 0; c0 < chains; c0 += wave) {
@@ -445,16 +484,22 @@ static void launch_cfg(const PassArgs& a, int vertical, int nframes, int wave_ch
     }
 }
 
+template <int LPL, bool PAD, bool WIN>
+static void launch_first(const PassArgs& a, int vertical, int nframes, int wave, cudaStream_t s) {
+    if (a.first && !vertical) launch_cfg<LPL, PAD, WIN, true>(a, vertical, nframes, wave, s);
+    else launch_cfg<LPL, PAD, WIN, false>(a, vertical, nframes, wave, s);
+}
+
 template <int LPL>
 static void launch_lpl(const PassArgs& a, int vertical, int nframes, int wave, cudaStream_t s) {
     const bool pad = a.L.K != 32 * LPL;
     const bool win = a.T <= LPL + 1;
     if (pad) {
-        if (win) launch_cfg<LPL, true, true>(a, vertical, nframes, wave, s);
-        else launch_cfg<LPL, true, false>(a, vertical, nframes, wave, s);
+        if (win) launch_first<LPL, true, true>(a, vertical, nframes, wave, s);
+        else launch_first<LPL, true, false>(a, vertical, nframes, wave, s);
     } else {
-        if (win) launch_cfg<LPL, false, true>(a, vertical, nframes, wave, s);
-        else launch_cfg<LPL, false, false>(a, vertical, nframes, wave, s);
+        if (win) launch_first<LPL, false, true>(a, vertical, nframes, wave, s);
+        else launch_first<LPL, false, false>(a, vertical, nframes, wave, s);
     }
 }
 

@@ -1,17 +1,13 @@
 // hm_device.cuh -- device primitives of the chain DP shared by the Dual MM
 // half-step kernels (hm.cu) and the primitive entry points (primitives.cu):
-// register-vector loads / stores, cp.async helpers and Msg (Eq. msg-pass
-// P:663-667; Msg of Alg.5).
+// register-vector loads / stores, compact K-vector records, TMA bulk copies
+// with mbarriers, and Msg (Eq. msg-pass; Msg of Alg.5).
 #pragma once
 #include <climits>
 
 #include "dmm_internal.cuh"
 
 namespace dmm {
-
-constexpr int kCMax = 12;    // longest leaf block (nodes)
-constexpr int kDepth = 4;    // pending right pieces in a leaf block (ceil(log2 kCMax))
-constexpr int kRing = 8;     // cp.async ring slots per warp
 
 // ------------------------------------------------------------ small helpers
 template <int LPL>
@@ -75,13 +71,87 @@ __device__ __forceinline__ void st_u8(uint8_t* p, const int (&v)[LPL]) {
     }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+// ---- compact records: u16 v[KP] | int32 base | pad  (value = base + v)
+template <int LPL>
+__device__ __forceinline__ void ld_rec(const uint8_t* rec, int lane, int (&F)[LPL]) {
+    constexpr int KP = 32 * LPL;
+    const int base = *reinterpret_cast<const int32_t*>(rec + 2 * KP);
+    const uint8_t* p = rec + 2 * LPL * lane;
+    if constexpr (LPL == 1) {
+        F[0] = base + *reinterpret_cast<const uint16_t*>(p);
+    } else {
+        unsigned w[LPL / 2];
+        if constexpr (LPL == 2) {
+            w[0] = *reinterpret_cast<const unsigned*>(p);
+        } else if constexpr (LPL == 4) {
+            uint2 t = *reinterpret_cast<const uint2*>(p);
+            w[0] = t.x; w[1] = t.y;
+        } else {
+            uint4 t = *reinterpret_cast<const uint4*>(p);
+            w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+        }
+#pragma unroll
+        for (int q = 0; q < LPL / 2; ++q) {
+            F[2 * q] = base + (int)(w[q] & 0xffffu);
+            F[2 * q + 1] = base + (int)(w[q] >> 16);
+        }
+    }
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Store v (labels >= K ignored) as a record; base = min over labels < K.
+template <int LPL, bool PAD>
+__device__ __forceinline__ void st_rec(uint8_t* rec, int lane, const int (&v)[LPL], int K) {
+    constexpr int KP = 32 * LPL;
+    int lmin = INT_MAX;
+#pragma unroll
+    for (int e = 0; e < LPL; ++e)
+        if (!PAD || lane * LPL + e < K) lmin = min(lmin, v[e]);
+    const int base = __reduce_min_sync(kFull, lmin);
+    unsigned u[LPL];
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) u[e] = (!PAD || lane * LPL + e < K) ? (unsigned)(v[e] - base) : 0u;
+    uint8_t* p = rec + 2 * LPL * lane;
+    if constexpr (LPL == 1) {
+        *reinterpret_cast<uint16_t*>(p) = (uint16_t)u[0];
+    } else if constexpr (LPL == 2) {
+        *reinterpret_cast<unsigned*>(p) = u[0] | (u[1] << 16);
+    } else if constexpr (LPL == 4) {
+        *reinterpret_cast<uint2*>(p) = make_uint2(u[0] | (u[1] << 16), u[2] | (u[3] << 16));
+    } else {
+        *reinterpret_cast<uint4*>(p) =
+            make_uint4(u[0] | (u[1] << 16), u[2] | (u[3] << 16), u[4] | (u[5] << 16), u[6] | (u[7] << 16));
+    }
+    if (lane == 0) *reinterpret_cast<int32_t*>(rec + 2 * KP) = base;
+}
+
+// ---- TMA bulk copies (cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
 
 // ------------------------------------------------------------------- Msg
 // Generic exact distance transform on a warp-held K-vector:

@@ -56,12 +56,16 @@ def test_host_only_calls_without_gpu(lib):
     cfg = dmm.DmmConfig(1242, 375, 0, 127, 2, 3, 3, 4, 4, -1, 1, 4)
     n = L.dmm_workspace_bytes(ctypes.byref(cfg))
     px, cells = 1242 * 375, 1242 * 375 * 128
-    assert n >= cells * (1 + 4 * 4) + px * 11
+    rec = 2 * 128 + 16                 # compact u16-span dual record per pixel
+    assert n >= cells * (1 + 2 * 4) + 2 * px * rec + px * 11
     bad = dmm.DmmConfig(1242, 375, 0, 300, 2, 3, 3, 4, 4, -1, 1, 4)   # K > 256
     assert L.dmm_workspace_bytes(ctypes.byref(bad)) == 0
     h = ctypes.c_void_p()
     assert L.dmm_create(ctypes.byref(bad), None, 0, 0, ctypes.byref(h)) == 1   # DMM_E_ARG
     assert L.dmm_status_str(3) == b"invalid state"
+    # span bound (2*w*min(T,K-1) + maxD) * 2^F > 65535 -> DMM_E_RANGE (6)
+    big = dmm.DmmConfig(64, 32, 0, 63, 2, 255, 255, 63, 8, -1, 1, 4)
+    assert L.dmm_create(ctypes.byref(big), ctypes.c_void_p(256), 1 << 40, 0, ctypes.byref(h)) == 6
     assert L.dmm_launch_count(None) == 0
 
 
