@@ -46,6 +46,7 @@ def traffic_per_launch():
     """dram__bytes_read.sum + dram__bytes_write.sum per hm_kernel launch from the
     committed ncu --set full capture summary (profiles/), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    # written from the latest committed ncu --set full capture (see profiles/README.md)
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f).get("hm_kernel_bytes_per_launch")
@@ -245,7 +246,16 @@ def main():
     hbm, peak_kind = peaks()
     ms_h, n_h = prof["hm_h"]
     ms_v, n_v = prof["hm_v"]
-    alg_bytes_per_step = cells * (5 + 9 * (iters - 1) + 8 * iters)
+    # compact dual records (u16 spans + int32 base,
+    # REC = 2*KP + 16 bytes per pixel) and the u8 cost volume, each input read
+    # once and each output written once per half-step:
+    #   H_1: D + f_ rec;  H_t: (D*2^F + g_) rec + D + f_ rec;  V: f_ rec + D + (D*2^F + g_) rec
+    KP = 32 * max(1, (K + 31) // 32)
+    while KP < K:
+        KP *= 2
+    rec = (2 * KP + 16) * W * H
+    dbytes = KP * W * H
+    alg_bytes_per_step = (dbytes + rec) + (iters - 1) * (2 * rec + dbytes) + iters * (2 * rec + dbytes)
     achieved = alg_bytes_per_step * args.steps / ((ms_h + ms_v) / 1e3) / 1e9
     tr = traffic_per_launch()
     step_ms_prof = sum(v[0] for v in prof.values()) / args.steps
