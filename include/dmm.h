@@ -140,6 +140,36 @@ DMM_API dmm_status dmm_handshake(const int32_t* Fi, const int32_t* Fj, const int
                                  const int32_t* phiR, int32_t* phi_ij, int32_t* phi_ji, int count,
                                  int K, int32_t ws, int32_t T, void* stream);
 
+/* ---- building blocks for sharded solves (paper_1601_06274_b200/sharding.py)
+ *
+ * dmm_buffer_ptr: device address and size of one of a frame's arrays, and the
+ * bytes per pixel: DMM_BUF_D (u8 [H][W][KP] cost volume, KP = padded K),
+ * DMM_BUF_FV (records of f_, REC = 2*KP + 16 bytes per pixel, see DESIGN.md
+ * "Compact duals"), DMM_BUF_FH (records of D*2^F + g_), DMM_BUF_LABELS
+ * (u8 [H][W]), DMM_BUF_BOUNDS (int64 [2*max_iters]).
+ * dmm_import_cost_volume: load a dense device cost volume u8 [H][W][K] (e.g. a
+ * band sliced out of a full-frame context's dmm_copy_cost_volume) as the
+ * frame's D; afterwards the frame is ready for dmm_half_step / dmm_solve.
+ * dmm_half_step: one half-step of Algorithm 2 on frames
+ * [frame, frame+nframes): vertical = 0 runs the H half-step of iteration t
+ * (t = 0 reads D only: g_ = 0, reading R4), vertical = 1 the V half-step (on
+ * t = iterations-1 it writes the labelling); bound slot 2t+vertical is reset
+ * and accumulated.  The V half-step reads the FV records, the H half-step
+ * (t > 0) the FH records, so a caller may exchange those between half-steps.
+ * dmm_energy: primal energy (Eq.3, scaled by 2^F) of the frame's current
+ * labels; synchronises `stream` and writes *energy. */
+#define DMM_BUF_D 0
+#define DMM_BUF_FV 1
+#define DMM_BUF_FH 2
+#define DMM_BUF_LABELS 3
+#define DMM_BUF_BOUNDS 4
+DMM_API dmm_status dmm_buffer_ptr(dmm_ctx* ctx, int frame, int which, void** ptr, size_t* bytes,
+                                  int* bytes_per_pixel);
+DMM_API dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* D_dense, void* stream);
+DMM_API dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int vertical,
+                                 int32_t iterations, void* stream);
+DMM_API dmm_status dmm_energy(dmm_ctx* ctx, int frame, int64_t* energy, void* stream);
+
 /* Number of kernels this context has launched since creation. */
 DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
 

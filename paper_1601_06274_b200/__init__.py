@@ -26,7 +26,9 @@ EXPORTS = (
     "dmm_result", "dmm_copy_labels", "dmm_copy_codes", "dmm_copy_cost_volume", "dmm_copy_dual",
     "dmm_run_host", "dmm_launch_count", "dmm_status_str", "dmm_last_error",
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
+    "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
 )
+BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
 TUNE_WAVE_BYTES = 1
 PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
 
@@ -76,6 +78,11 @@ def load_library():
         "dmm_set_tuning": (ctypes.c_int, [P, ctypes.c_int, i64]),
         "dmm_msg": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, i32, i32, P]),
         "dmm_handshake": (ctypes.c_int, [P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, i32, i32, P]),
+        "dmm_buffer_ptr": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P),
+                                          ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_int)]),
+        "dmm_import_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P]),
+        "dmm_half_step": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, i32, ctypes.c_int, i32, P]),
+        "dmm_energy": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(i64), P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -83,6 +90,11 @@ def load_library():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def torch_int64():
+    import torch
+    return torch.int64
 
 
 def _stream_handle(stream) -> int:
@@ -245,6 +257,45 @@ class Context:
         out = torch.empty((self.H, self.W, self.K), dtype=torch.int32, device=self.device)
         self._call("dmm_copy_dual", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
         return out
+
+    # ------------------------------------------------ sharding building blocks
+    def buffer(self, which: int, frame: int = 0):
+        """uint8 CUDA tensor view (H, W, bytes_per_pixel) of one of the frame's
+        arrays inside the workspace (BUF_D, BUF_FV, BUF_FH, BUF_LABELS)."""
+        ptr = ctypes.c_void_p()
+        nbytes = ctypes.c_size_t()
+        bpp = ctypes.c_int()
+        self._call("dmm_buffer_ptr", frame, which, ctypes.byref(ptr), ctypes.byref(nbytes), ctypes.byref(bpp))
+        off = ptr.value - self.workspace.data_ptr()
+        flat = self.workspace[off: off + nbytes.value]
+        if which == BUF_BOUNDS:
+            return flat.view(torch_int64())
+        return flat.view(self.H, self.W, max(bpp.value, 1))
+
+    def import_cost_volume(self, D, frame: int = 0, stream=None):
+        """Load a dense uint8 (H, W, K) CUDA tensor as the frame's cost volume."""
+        D = D.contiguous()
+        if tuple(D.shape) != (self.H, self.W, self.K):
+            raise DmmError(f"cost volume shape {tuple(D.shape)} != {(self.H, self.W, self.K)}")
+        self._call("dmm_import_cost_volume", frame, ctypes.c_void_p(D.data_ptr()), _stream_handle(stream))
+        self._iters[frame] = 0
+
+    def half_step(self, t: int, vertical: int, iterations: int, frame: int = 0, nframes: int = 1, stream=None):
+        """One half-step of Algorithm 2 (H if vertical == 0, else V) of iteration t."""
+        self._call("dmm_half_step", frame, nframes, t, vertical, iterations, _stream_handle(stream))
+        if vertical and t == iterations - 1:
+            for f in range(frame, frame + nframes):
+                self._iters[f] = iterations
+
+    def bound_slots(self, frame: int = 0):
+        """int64 CUDA tensor view of the frame's bound history slots."""
+        return self.buffer(BUF_BOUNDS, frame)
+
+    def energy(self, frame: int = 0, stream=None) -> int:
+        """Primal energy (scaled by 2**frac_bits) of the frame's current labels (synchronises)."""
+        e = ctypes.c_int64()
+        self._call("dmm_energy", frame, ctypes.byref(e), _stream_handle(stream))
+        return int(e.value)
 
     def run_host(self, left, right, iterations: int = 4, labels_out=None, frame: int = 0, stream=None):
         """End-to-end through the C ABI with HOST buffers (numpy or CPU tensors,

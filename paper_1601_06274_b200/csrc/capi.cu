@@ -127,6 +127,31 @@ dmm_status frame_ok(dmm_ctx* ctx, int frame, int n = 1) {
     return DMM_OK;
 }
 
+// One half-step (vertical = 0: H, 1: V) of iteration t on frames [frame, frame+nframes).
+void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations, cudaStream_t s) {
+    const int T = ctx->cfg.trunc < ctx->K ? ctx->cfg.trunc : ctx->K;   // T >= K: untruncated
+    dmm::PassArgs a;
+    a.L = ctx->L;
+    a.frame0 = frame;
+    a.fbits = ctx->cfg.frac_bits;
+    a.ws = (v ? ctx->cfg.w_v : ctx->cfg.w_h) << ctx->cfg.frac_bits;
+    a.wsT = a.ws * T;
+    a.T = T;
+    a.first = (t == 0 && v == 0);
+    a.last = (t == iterations - 1 && v == 1);
+    a.bound_slot = 2 * t + v;
+    // optional L2-sized waves: the node records of one wave fit the budget
+    const int chains = v ? ctx->L.W : ctx->L.H;
+    const size_t per_chain = (size_t)(v ? ctx->L.H : ctx->L.W) * dmm::rec_bytes(ctx->KP) * nframes;
+    int wave = 0;
+    if (ctx->wave_budget > 0) {
+        const size_t nw = (per_chain * chains + ctx->wave_budget - 1) / ctx->wave_budget;
+        if (nw > 1) wave = (int)((chains + nw - 1) / nw);
+    }
+    Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
+    dmm::launch_hm_pass(a, v, nframes, wave, s);
+}
+
 }  // namespace
 
 extern "C" {
@@ -224,29 +249,9 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
                            "memset bounds")))
             return st;
     }
-    const int T = ctx->cfg.trunc < ctx->K ? ctx->cfg.trunc : ctx->K;   // T >= K: untruncated
     for (int t = 0; t < iterations; ++t) {
         for (int v = 0; v < 2; ++v) {
-            dmm::PassArgs a;
-            a.L = ctx->L;
-            a.frame0 = frame;
-            a.fbits = ctx->cfg.frac_bits;
-            a.ws = (v ? ctx->cfg.w_v : ctx->cfg.w_h) << ctx->cfg.frac_bits;
-            a.wsT = a.ws * T;
-            a.T = T;
-            a.first = (t == 0 && v == 0);
-            a.last = (t == iterations - 1 && v == 1);
-            a.bound_slot = 2 * t + v;
-            // L2-sized waves: chain data (F records) of one wave fits the budget
-            const int chains = v ? ctx->L.W : ctx->L.H;
-            const size_t per_chain = (size_t)(v ? ctx->L.H : ctx->L.W) * ctx->KP * (v ? 4 : 5) * nframes;
-            int wave = 0;
-            if (ctx->wave_budget > 0) {
-                const size_t nw = (per_chain * chains + ctx->wave_budget - 1) / ctx->wave_budget;
-                if (nw > 1) wave = (int)((chains + nw - 1) / nw);
-            }
-            Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
-            dmm::launch_hm_pass(a, v, nframes, wave, s);
+            launch_half(ctx, frame, nframes, t, v, iterations, s);
             if (ctx->stop_after_h) break;
         }
         if (ctx->stop_after_h) break;
@@ -347,6 +352,86 @@ dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const
     if ((st = cuda_err(ctx, cudaMemcpyAsync(labels_host, P.labels, px, cudaMemcpyDeviceToHost, s), "d2h")))
         return st;
     return dmm_result(ctx, frame, energy, bound, nullptr, stream);
+}
+
+dmm_status dmm_buffer_ptr(dmm_ctx* ctx, int frame, int which, void** ptr, size_t* bytes, int* bytes_per_pixel) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    const size_t px = (size_t)ctx->L.W * ctx->L.H;
+    void* p = nullptr;
+    int bpp = 0;
+    size_t n = 0;
+    switch (which) {
+        case DMM_BUF_D: p = P.D; bpp = ctx->KP; n = px * bpp; break;
+        case DMM_BUF_FV: p = P.fv; bpp = dmm::rec_bytes(ctx->KP); n = px * bpp; break;
+        case DMM_BUF_FH: p = P.fh; bpp = dmm::rec_bytes(ctx->KP); n = px * bpp; break;
+        case DMM_BUF_LABELS: p = P.labels; bpp = 1; n = px; break;
+        case DMM_BUF_BOUNDS: p = P.bounds; bpp = 0; n = 8 * 2 * (size_t)ctx->cfg.max_iters; break;
+        default: ctx->err = "unknown buffer"; return DMM_E_ARG;
+    }
+    if (ptr) *ptr = p;
+    if (bytes) *bytes = n;
+    if (bytes_per_pixel) *bytes_per_pixel = bpp;
+    return DMM_OK;
+}
+
+dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* D_dense, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!D_dense) return DMM_E_ARG;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    dmm::launch_pad_u8(D_dense, P.D, (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
+    if ((st = check_launch(ctx, "import cost volume"))) return st;
+    ctx->has_cost[frame] = 1;
+    ctx->iters_done[frame] = 0;
+    return DMM_OK;
+}
+
+dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int vertical, int32_t iterations,
+                         void* stream) {
+    dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st) return st;
+    if (iterations < 1 || iterations > ctx->cfg.max_iters || t < 0 || t >= iterations ||
+        (vertical != 0 && vertical != 1)) {
+        ctx->err = "bad half-step index";
+        return DMM_E_ARG;
+    }
+    for (int f = frame; f < frame + nframes; ++f)
+        if (!ctx->has_cost[f]) { ctx->err = "half step before cost volume"; return DMM_E_STATE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    {   // reset this half-step's bound slot of every frame
+        dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+        if ((st = cuda_err(ctx, cudaMemset2DAsync(P.bounds + 2 * t + vertical, ctx->L.frame_bytes, 0, 8,
+                                                  nframes, s),
+                           "memset bound slot")))
+            return st;
+    }
+    launch_half(ctx, frame, nframes, t, vertical, iterations, s);
+    if ((st = check_launch(ctx, "half step"))) return st;
+    if (vertical && t == iterations - 1)
+        for (int f = frame; f < frame + nframes; ++f) ctx->iters_done[f] = iterations;
+    return DMM_OK;
+}
+
+dmm_status dmm_energy(dmm_ctx* ctx, int frame, int64_t* energy, void* stream) {
+    dmm_status st = frame_ok(ctx, frame);
+    if (st) return st;
+    if (!energy) return DMM_E_ARG;
+    if (!ctx->has_cost[frame]) { ctx->err = "energy before cost volume"; return DMM_E_STATE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    long long e = 0;
+    if ((st = cuda_err(ctx, cudaMemsetAsync(P.energy, 0, 8, s), "memset energy"))) return st;
+    {
+        Timed tm(ctx, 4, s);
+        dmm::launch_energy(ctx->L, frame, 1, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc, ctx->cfg.frac_bits, s);
+    }
+    if ((st = check_launch(ctx, "energy"))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(&e, P.energy, 8, cudaMemcpyDeviceToHost, s), "d2h"))) return st;
+    if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
+    *energy = e;
+    return DMM_OK;
 }
 
 int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }

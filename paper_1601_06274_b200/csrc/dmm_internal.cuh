@@ -91,6 +91,8 @@ int hm_launches_per_pass(const PassArgs& a, int vertical, int wave);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
+// dense u8 [cells][K] -> padded [cells][KP] (pads = 0)
+void launch_pad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
 // Expand compact records to dense int32 [cells][K]; if D != nullptr subtract
 // D*2^fbits (recovers g_ from fh).
 void launch_decode_rec(const uint8_t* rec, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K,

@@ -49,6 +49,21 @@ __global__ void unpad_kernel(const T* __restrict__ src, T* __restrict__ dst, lon
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s) {
     unpad_kernel<uint8_t><<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
 }
+__global__ void pad_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, long long cells, int K,
+                           int KP) {
+    const long long n = cells * KP;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / KP;
+        const int k = (int)(i - c * KP);
+        dst[i] = k < K ? src[c * K + k] : 0;
+    }
+}
+
+void launch_pad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s) {
+    pad_kernel<<<4 * 148, 256, 0, s>>>(src, dst, cells, K, KP);
+}
+
 __global__ void decode_rec_kernel(const uint8_t* __restrict__ rec, const uint8_t* __restrict__ D, int fbits,
                                   int32_t* __restrict__ dst, long long cells, int K, int KP) {
     const int R = rec_bytes(KP);

@@ -193,3 +193,44 @@ def test_handshake_primitive(orc, K):
             pij = orc.msg(np.floor_divide(m - 2 * pji, 2), ws, T)
             pji2 = orc.msg(-pij, ws, T)
             assert np.array_equal(gij[v].cpu().numpy(), pij) and np.array_equal(gji[v].cpu().numpy(), pji2)
+
+
+# ------------------------------------------------------- band sharding (8e)
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_band_sharded_lockstep_equals_unsharded(orc, world):
+    """Row/column band decomposition on the CUDA path (all ranks' contexts in
+    one process, transposes as data movement): bit-identical to the
+    unsharded solve and to the oracle."""
+    from paper_1601_06274_b200 import sharding
+    W, H, K, iters = 131, 47, 64, 3
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=11)
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    engines = [sharding.CudaBandEngine(W, H, world, r, d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4,
+                                       max_iters=iters) for r in range(world)]
+    labels, hist, energy = sharding.solve_bands_lockstep(engines, lt, rt, iters)
+    o = _run_oracle(orc, left, right, 0, K, 3, 3, 4, 4, iters)
+    assert np.array_equal(labels.cpu().numpy().astype(np.int32), o["labels"])
+    assert np.array_equal(np.array(hist), o["bound_hist"])
+    assert energy == o["energy"]
+
+
+def test_primitive_buffers_and_half_steps(orc):
+    """dmm_half_step x 2*iters == dmm_solve (same records, bounds, labels)."""
+    W, H, K, iters = 70, 33, 32, 3
+    left, right, _ = datagen.pair("rd", W, H, K, seed=3)
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    import paper_1601_06274_b200 as dmm
+    a = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=iters)
+    b = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=iters)
+    a.cost_volume(lt, rt)
+    a.solve(iters)
+    b.import_cost_volume(a.cost_volume_tensor())
+    for t in range(iters):
+        b.half_step(t, 0, iters)
+        b.half_step(t, 1, iters)
+    torch.cuda.synchronize()
+    assert torch.equal(a.buffer(dmm.BUF_FV), b.buffer(dmm.BUF_FV))
+    assert torch.equal(a.buffer(dmm.BUF_FH), b.buffer(dmm.BUF_FH))
+    assert torch.equal(a.labels(), b.labels())
+    assert a.result()[2] == [int(v) for v in b.bound_slots()[: 2 * iters].tolist()]
+    assert a.result()[0] == b.energy()
