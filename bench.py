@@ -169,6 +169,9 @@ def main():
     ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", choices=("frames", "bands"), default="frames",
+                    help="frames: one frame per GPU (weak scaling); bands: one frame sharded in row/column "
+                         "bands with an all-to-all between half-steps (strong scaling)")
     ap.add_argument("--wave-mb", type=float, default=None,
                     help="L2 wave budget of the chain-DP launches in MiB (0 = one launch; default: library's)")
     args = ap.parse_args()
@@ -191,6 +194,8 @@ def main():
 
     c = datagen.CONFIGS[args.config]
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+    if args.mode == "bands":
+        return run_bands(args, c, world, rank, local, dev)
     left, right, _ = datagen.pair(c["kind"], W, H, K, seed=rank)   # one frame per rank
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
                       max_iters=iters, device=dev)
@@ -321,6 +326,59 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_bands(args, c, world, rank, local, dev):
+    """One frame sharded in row bands (H) / column bands (V) over all ranks,
+    all-to-all transposes over NCCL between half-steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1601_06274_b200 import sharding
+    W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+    left, right, _ = datagen.pair(c["kind"], W, H, K, seed=0)       # the same frame on every rank
+    if world == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29561")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    eng = sharding.CudaBandEngine(W, H, world, rank, d_min=0, d_max=K - 1, w=W_REG, T=T_REG,
+                                  frac_bits=FBITS, max_iters=iters, device=dev)
+    exch = sharding.DistExchanger()
+    lt = torch.from_numpy(left).to(dev)
+    rt = torch.from_numpy(right).to(dev)
+    for _ in range(args.warmup):
+        sharding.solve_bands(eng, exch, lt, rt, iters)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    t0.record()
+    for _ in range(args.steps):
+        labels, hist, energy = sharding.solve_bands(eng, exch, lt, rt, iters)
+    t1.record()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        cells = W * H * K
+        line = {
+            "metric": METRIC, "value": cells * iters / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: one {W}x{H}x{K} frame sharded in {world} row/column bands, "
+                                   f"{iters} dual iterations, all-to-all transposes between half-steps",
+                       "W": W, "H": H, "K": K, "iters": iters, "fps": 1e3 / ms, "parallelism": f"bands x{world}"},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "clocks": clocks,
+            "result": {"energy": energy / (1 << FBITS), "bound": hist[-1] / (1 << FBITS)},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

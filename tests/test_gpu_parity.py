@@ -229,8 +229,9 @@ def test_primitive_buffers_and_half_steps(orc):
         b.half_step(t, 0, iters)
         b.half_step(t, 1, iters)
     torch.cuda.synchronize()
-    assert torch.equal(a.buffer(dmm.BUF_FV), b.buffer(dmm.BUF_FV))
-    assert torch.equal(a.buffer(dmm.BUF_FH), b.buffer(dmm.BUF_FH))
+    # records' 12 pad bytes are never written: compare the decoded duals
+    assert torch.equal(a.dual(0), b.dual(0)) and torch.equal(a.dual(1), b.dual(1))
+    assert torch.equal(a.buffer(dmm.BUF_FV)[:, :, : 2 * 32 + 4], b.buffer(dmm.BUF_FV)[:, :, : 2 * 32 + 4])
     assert torch.equal(a.labels(), b.labels())
     assert a.result()[2] == [int(v) for v in b.bound_slots()[: 2 * iters].tolist()]
     assert a.result()[0] == b.energy()
