@@ -38,7 +38,7 @@ constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece st
 constexpr int kDepth = 4;    // pending right pieces in a leaf block (ceil(log2 kCMax))
 constexpr int kCH = 4;       // nodes per ring chunk (global kernel)
 constexpr int kNSlot = 4;    // ring chunks per warp (prefetch depth kNSlot * kCH nodes)
-constexpr int kNWG = 4;      // warps per CTA, global kernel
+constexpr int kNWG = 8;      // warps per CTA, level kernels
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -87,10 +87,15 @@ struct Pass {
     }
 };
 
-// ============================================================ global kernel
-struct GlobalShared {   // per-warp shared memory (bytes)
+// ============================================================ level kernels
+// Global levels (subchains longer than kCMax) run level-synchronously: one
+// launch per hierarchy level, one warp per (chain, subchain) task, no CTA
+// barriers (the launch boundary orders the levels).  A task runs one pass --
+// the direction whose boundary changed -- and the Handshake; the node records
+// stream through a per-warp TMA ring.
+struct RingShared {     // per-warp shared memory (bytes)
     int slot, ring, mbar, total;
-    __host__ __device__ GlobalShared(int KP) {
+    __host__ __device__ RingShared(int KP) {
         slot = kCH * rec_bytes(KP);
         ring = 0;
         mbar = align_up(ring + kNSlot * slot, 8);
@@ -98,64 +103,27 @@ struct GlobalShared {   // per-warp shared memory (bytes)
     }
 };
 
-// The warp's node consumption order in the global levels, as runs of
-// consecutive nodes: per task its pass (forward lo..i-1 or backward hi..j+1)
-// then the Handshake pair j, i.
-struct RunSeq {
-    int n, lstar, warp, nw, lev, s, phase;
-    bool done;
-    __device__ __forceinline__ void init(int n_, int lstar_, int warp_, int nw_) {
-        n = n_; lstar = lstar_; warp = warp_; nw = nw_; lev = 0; s = warp_; phase = 0; done = false;
-    }
-    __device__ __forceinline__ bool next(int& start, int& dir, int& count) {
-        while (!done) {
-            if (lev >= lstar) { done = true; break; }
-            if (lev == 0) {
-                if (s > 1) { ++lev; s = warp; phase = 0; continue; }
-                const int i = n / 2 - 1, j = i + 1;
-                if (s == 0) {
-                    if (phase == 0) { phase = 1; start = 0; dir = 1; count = i; if (count > 0) return true; continue; }
-                    phase = 0; s += nw; start = j; dir = -1; count = 2; return true;
-                }
-                phase = 0; s += nw; start = n - 1; dir = -1; count = n - 1 - j;
-                if (count > 0) return true;
-                continue;
-            }
-            if (s >= (1 << lev)) { ++lev; s = warp; phase = 0; continue; }
-            int lo, hi;
-            task_bounds(n, lev, s, lo, hi);
-            const int i = lo + (hi - lo + 1) / 2 - 1, j = i + 1;
-            if (phase == 0) {
-                phase = 1;
-                if (!(s & 1)) { start = hi; dir = -1; count = hi - j; }
-                else { start = lo; dir = 1; count = i - lo; }
-                if (count > 0) return true;
-                continue;
-            }
-            phase = 0; s += nw; start = j; dir = -1; count = 2; return true;
-        }
-        return false;
-    }
-};
-
 template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
-struct Glob : Pass<LPL, VERT, PAD, WIN, FIRST> {
+struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
     using B = Pass<LPL, VERT, PAD, WIN, FIRST>;
     using B::KP; using B::REC; using B::SREC;
     uint8_t* ring;
     uint64_t* mbar;
     int slotB;
-    RunSeq seq;
+    // the task's runs: 0 = its pass, 1 = the Handshake pair (j, i) (absent for the root's bwd warp)
+    int rs0, rd0, rc0, rs1, rd1, rc1, nruns, cur;
     int r_start, r_dir, r_left;     // producer: rest of the current run
     unsigned clen;                  // chunk length of slot s in bits 8s..8s+7 (per-lane copy)
     int cslot, cidx, ccount;        // consumer position
-    unsigned cphase;                // consumer parity bit per slot
+    unsigned cphase;                // consumer parity bit per slot (kept across tasks)
     bool cwait;
 
-    // ---- producer: fill `slot` with the next chunk (<= kCH nodes of one run)
     __device__ __forceinline__ void fill(int slot) {
         while (r_left == 0) {
-            if (!seq.next(r_start, r_dir, r_left)) return;
+            if (cur >= nruns) return;
+            if (cur == 0) { r_start = rs0; r_dir = rd0; r_left = rc0; }
+            else { r_start = rs1; r_dir = rd1; r_left = rc1; }
+            ++cur;
         }
         const int cnt = r_left < kCH ? r_left : kCH;
         uint8_t* sbase = ring + slot * slotB;
@@ -171,7 +139,7 @@ struct Glob : Pass<LPL, VERT, PAD, WIN, FIRST> {
         r_start += r_dir * cnt;
         r_left -= cnt;
     }
-    __device__ __forceinline__ void ring_init(char* wsm, const GlobalShared& lay, int lstar, int warp) {
+    __device__ __forceinline__ void ring_init(char* wsm, const RingShared& lay) {
         ring = reinterpret_cast<uint8_t*>(wsm + lay.ring);
         mbar = reinterpret_cast<uint64_t*>(wsm + lay.mbar);
         slotB = lay.slot;
@@ -180,12 +148,14 @@ struct Glob : Pass<LPL, VERT, PAD, WIN, FIRST> {
             fence_mbar_init();
         }
         __syncwarp();
-        seq.init(this->n, lstar, warp, kNWG);
-        r_left = 0; clen = 0;
-        cslot = 0; cidx = 0; ccount = 0; cphase = 0; cwait = true;
+        cphase = 0;
+    }
+    // start streaming a task's runs (the previous task's chunks are all consumed)
+    __device__ __forceinline__ void start(int nr) {
+        nruns = nr; cur = 0; r_left = 0; clen = 0;
+        cslot = 0; cidx = 0; ccount = 0; cwait = true;
         for (int k = 0; k < kNSlot; ++k) fill(k);
     }
-    // ---- consumer: next node's F
     __device__ __forceinline__ void pop(int (&F)[LPL]) {
         if (cwait) {
             mbar_wait(&mbar[cslot], (cphase >> cslot) & 1u);
@@ -203,8 +173,7 @@ struct Glob : Pass<LPL, VERT, PAD, WIN, FIRST> {
             cwait = true;
         }
     }
-
-    // ---- passes (messages in the fwd/bwd scratch arrays)
+    // ---- passes (spine messages to the fwd/bwd scratch arrays)
     __device__ __forceinline__ void pass_fwd(int lo, int end, int (&phi)[LPL]) {
         const int len0 = end - lo + 1;
         if (len0 < 2) return;
@@ -255,69 +224,78 @@ struct Glob : Pass<LPL, VERT, PAD, WIN, FIRST> {
     }
 };
 
-// Levels 0 .. lstar-1 of every chain's hierarchy; leaves the boundary messages
-// of every leaf block in the fwd/bwd scratch.
+// Level 0: the whole chain [0, n-1] with zero boundary messages; warp 0 runs the
+// forward pass into i, warp 1 the backward pass into j, warp 0 the Handshake.
 template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
-__global__ void __launch_bounds__(kNWG * 32) hm_global_kernel(PassArgs a, int lstar) {
+__global__ void __launch_bounds__(64) hm_root_kernel(PassArgs a) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
-    const GlobalShared lay(KP);
-    Glob<LPL, VERT, PAD, WIN, FIRST> h;
+    const RingShared lay(KP);
+    Task<LPL, VERT, PAD, WIN, FIRST> h;
     h.init(a, blockIdx.x, lane);
-    h.ring_init(smem + warp * lay.total, lay, lstar, warp);
-    const int n = h.n;
-    int zero[LPL];
+    h.ring_init(smem + warp * lay.total, lay);
+    const int n = h.n, i = n / 2 - 1, j = i + 1;
+    int zero[LPL], phi[LPL];
 #pragma unroll
-    for (int e = 0; e < LPL; ++e) zero[e] = 0;
-
-    // ---- level 0: the whole chain, zero boundary messages
-    const int i = n / 2 - 1;
-    int pl[LPL], pr[LPL];
-#pragma unroll
-    for (int e = 0; e < LPL; ++e) { pl[e] = 0; pr[e] = 0; }
-    if (warp == 0) { st_i32<LPL>(h.P.fwd + h.moff(0), zero); h.pass_fwd(0, i, pl); }
-    if (warp == 1) {
+    for (int e = 0; e < LPL; ++e) { zero[e] = 0; phi[e] = 0; }
+    if (warp == 0) {
+        h.rs0 = 0; h.rd0 = 1; h.rc0 = i;
+        h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
+        h.start(2);
+        st_i32<LPL>(h.P.fwd + h.moff(0), zero);
+        h.pass_fwd(0, i, phi);
+    } else {
+        h.rs0 = n - 1; h.rd0 = -1; h.rc0 = n - 1 - j;
+        h.start(1);
         st_i32<LPL>(h.P.bwd + h.moff(n - 1), zero);
-        h.pass_bwd(n - 1, i + 1, pr);
-        st_i32<LPL>(h.P.bwd + h.moff(i + 1), pr);
+        h.pass_bwd(n - 1, j, phi);
+        st_i32<LPL>(h.P.bwd + h.moff(j), phi);
     }
     __syncthreads();
     if (warp == 0) {
-        ld_i32<LPL>(h.P.bwd + h.moff(i + 1), pr);
-        h.handshake(i, pl, pr);
+        int pr[LPL];
+        ld_i32<LPL>(h.P.bwd + h.moff(j), pr);
+        h.handshake(i, phi, pr);
     }
-    __syncthreads();
-    // ---- levels 1 .. lstar-1; message loads issued one task ahead
+}
+
+// Level lev >= 1: one warp per (chain, subchain s) task.
+template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST, int NW>
+__global__ void __launch_bounds__(NW * 32) hm_level_kernel(PassArgs a, int lev, int ntasks) {
+    extern __shared__ __align__(128) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int KP = 32 * LPL;
+    const RingShared lay(KP);
+    Task<LPL, VERT, PAD, WIN, FIRST> h;
+    h.init(a, 0, lane);
+    h.ring_init(smem + warp * lay.total, lay);
+    const int n = h.n;
 #pragma unroll 1
-    for (int lev = 1; lev < lstar; ++lev) {
-        int nb_[LPL], ns_[LPL];    // next task's boundary and spine messages
-        auto load_msgs = [&](int s, int (&bnd)[LPL], int (&spn)[LPL]) {
-            int lo, hi;
-            task_bounds(n, lev, s, lo, hi);
-            const int ii = lo + (hi - lo + 1) / 2 - 1;
-            if (!(s & 1)) { ld_i32<LPL>(h.P.bwd + h.moff(hi), bnd); ld_i32<LPL>(h.P.fwd + h.moff(ii), spn); }
-            else { ld_i32<LPL>(h.P.fwd + h.moff(lo), bnd); ld_i32<LPL>(h.P.bwd + h.moff(ii + 1), spn); }
-        };
-        if (warp < (1 << lev)) load_msgs(warp, nb_, ns_);
-#pragma unroll 1
-        for (int s = warp; s < (1 << lev); s += kNWG) {
-            int bnd[LPL], spn[LPL];
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) { bnd[e] = nb_[e]; spn[e] = ns_[e]; }
-            if (s + kNWG < (1 << lev)) load_msgs(s + kNWG, nb_, ns_);
-            int lo, hi;
-            task_bounds(n, lev, s, lo, hi);
-            const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
-            if (!(s & 1)) {   // left piece: left boundary kept -> reuse fwd, recompute bwd
-                h.pass_bwd(hi, j, bnd);
-                h.handshake(ii, spn, bnd);
-            } else {          // right piece: right boundary kept -> reuse bwd, recompute fwd
-                h.pass_fwd(lo, ii, bnd);
-                h.handshake(ii, bnd, spn);
-            }
+    for (int t = blockIdx.x * NW + warp; t < ntasks; t += gridDim.x * NW) {
+        h.c = t >> lev;
+        const int s = t & ((1 << lev) - 1);
+        int lo, hi;
+        task_bounds(n, lev, s, lo, hi);
+        const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
+        int bnd[LPL], spn[LPL];
+        if (!(s & 1)) {   // left piece: left boundary kept -> reuse fwd, recompute bwd
+            h.rs0 = hi; h.rd0 = -1; h.rc0 = hi - j;
+            h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
+            h.start(2);
+            ld_i32<LPL>(h.P.bwd + h.moff(hi), bnd);
+            ld_i32<LPL>(h.P.fwd + h.moff(ii), spn);
+            h.pass_bwd(hi, j, bnd);
+            h.handshake(ii, spn, bnd);
+        } else {          // right piece: right boundary kept -> reuse bwd, recompute fwd
+            h.rs0 = lo; h.rd0 = 1; h.rc0 = ii - lo;
+            h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
+            h.start(2);
+            ld_i32<LPL>(h.P.fwd + h.moff(lo), bnd);
+            ld_i32<LPL>(h.P.bwd + h.moff(j), spn);
+            h.pass_fwd(lo, ii, bnd);
+            h.handshake(ii, bnd, spn);
         }
-        __syncthreads();
     }
 }
 
@@ -490,11 +468,25 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     const int chains = VERT ? a.L.W : a.L.H;
     const int n = VERT ? a.L.H : a.L.W;
     const int lstar = leaf_level(n);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (lstar > 0) {
-        const int smem = kNWG * GlobalShared(KP).total;
-        auto kern = hm_global_kernel<LPL, VERT, PAD, WIN, FIRST>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        kern<<<dim3(chains, nframes), kNWG * 32, smem, s>>>(a, lstar);
+        const int rs = RingShared(KP).total;
+        auto rk = hm_root_kernel<LPL, VERT, PAD, WIN, FIRST>;
+        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * rs);
+        rk<<<dim3(chains, nframes), 64, 2 * rs, s>>>(a);
+        auto lk = hm_level_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
+        cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNWG * rs);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, kNWG * 32, kNWG * rs);
+        const int cap = sms * (per_sm > 0 ? per_sm : 1);
+        for (int lev = 1; lev < lstar; ++lev) {
+            const int ntasks = chains << lev;
+            int grid = (ntasks + kNWG - 1) / kNWG;
+            if (grid > cap) grid = cap;
+            lk<<<dim3(grid, nframes), kNWG * 32, kNWG * rs, s>>>(a, lev, ntasks);
+        }
     }
     const int smem = kNWL * LeafShared(KP).total;
     auto kern = hm_leaf_kernel<LPL, VERT, PAD, WIN, FIRST>;
@@ -502,9 +494,6 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     const int nblocks = chains << lstar;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNWL * 32, smem);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = (nblocks + kNWL - 1) / kNWL;
     const int cap = sms * (per_sm > 0 ? per_sm : 1);
     if (grid > cap) grid = cap;
@@ -533,7 +522,7 @@ static void launch_lpl(const PassArgs& a, int vertical, int nframes, cudaStream_
 
 int hm_launches_per_pass(const PassArgs& a, int vertical, int /*wave*/) {
     const int n = vertical ? a.L.H : a.L.W;
-    return leaf_level(n) > 0 ? 2 : 1;
+    return leaf_level(n) + 1;      // root + levels 1..l*-1 + leaf blocks
 }
 
 void launch_hm_pass(const PassArgs& a, int vertical, int nframes, int /*wave*/, cudaStream_t s) {
