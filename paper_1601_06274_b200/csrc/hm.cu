@@ -36,8 +36,6 @@ namespace dmm {
 
 constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
 constexpr int kDepth = 4;    // pending right pieces in a leaf block (ceil(log2 kCMax))
-constexpr int kCH = 4;       // nodes per ring chunk (global kernel)
-constexpr int kNSlot = 4;    // ring chunks per warp (prefetch depth kNSlot * kCH nodes)
 constexpr int kNWG = 8;      // warps per CTA, level kernels
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
 
@@ -53,7 +51,7 @@ __device__ __forceinline__ void task_bounds(int n, int lev, int s, int& lo, int&
 }
 
 // Per-pass constants shared by both kernels.
-template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
 struct Pass {
     static constexpr int KP = 32 * LPL;
     static constexpr int REC = rec_bytes(KP);
@@ -75,14 +73,14 @@ struct Pass {
     __device__ __forceinline__ int q_of(int p) const { return VERT ? p * W + c : c * W + p; }
     __device__ __forceinline__ size_t moff(int p) const { return (size_t)q_of(p) * KP + lane * LPL; }
     __device__ __forceinline__ void msg_(int (&x)[LPL]) const { msg<LPL, PAD, WIN>(x, ws, wsT, lane, K); }
-    // decode a staged source record: F (and the D row when it is the record)
-    __device__ __forceinline__ void dec(const uint8_t* rec, int (&F)[LPL]) const {
+    // decode a staged source record at shared address `rec`: F (FIRST: D*2^F)
+    __device__ __forceinline__ void dec(unsigned rec, int (&F)[LPL]) const {
         if constexpr (FIRST) {
-            ld_u8<LPL>(rec + lane * LPL, F);
+            ld_u8_s<LPL>(rec + lane * LPL, F);
 #pragma unroll
             for (int e = 0; e < LPL; ++e) F[e] <<= fbits;
         } else {
-            ld_rec<LPL>(rec, lane, F);
+            ld_rec_s<LPL>(rec, lane, F);
         }
     }
 };
@@ -93,28 +91,34 @@ struct Pass {
 // barriers (the launch boundary orders the levels).  A task runs one pass --
 // the direction whose boundary changed -- and the Handshake; the node records
 // stream through a per-warp TMA ring.
-struct RingShared {     // per-warp shared memory (bytes)
+template <int CH, int NS>
+struct RingShared {     // per-warp shared memory (bytes): NS chunks of CH records
     int slot, ring, mbar, total;
     __host__ __device__ RingShared(int KP) {
-        slot = kCH * rec_bytes(KP);
+        slot = CH * rec_bytes(KP);
         ring = 0;
-        mbar = align_up(ring + kNSlot * slot, 8);
-        total = align_up(mbar + kNSlot * 8, 128);
+        mbar = align_up(ring + NS * slot, 8);
+        total = align_up(mbar + NS * 8, 128);
     }
 };
+// ring geometry: the root's two passes per chain are the latency-critical path
+// with few warps per SM, so they prefetch deepest (64 nodes)
+constexpr int kRootCH = 8, kRootNS = 8;
+constexpr int kLevCH = 4, kLevNS = 8;
 
-template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int kCH, int kNSlot>
 struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
     using B = Pass<LPL, VERT, PAD, WIN, FIRST>;
     using B::KP; using B::REC; using B::SREC;
-    uint8_t* ring;
-    uint64_t* mbar;
+    unsigned ring;                  // shared address of the ring
+    unsigned mbar;                  // shared address of the NS mbarriers (8 B each)
     int slotB;
     // the task's runs: 0 = its pass, 1 = the Handshake pair (j, i) (absent for the root's bwd warp)
     int rs0, rd0, rc0, rs1, rd1, rc1, nruns, cur;
     int r_start, r_dir, r_left;     // producer: rest of the current run
-    unsigned clen;                  // chunk length of slot s in bits 8s..8s+7 (per-lane copy)
+    unsigned long long clen;        // chunk length of slot s in bits 8s..8s+7 (per-lane copy)
     int cslot, cidx, ccount;        // consumer position
+    bool crev;                      // current chunk holds a descending run
     unsigned cphase;                // consumer parity bit per slot (kept across tasks)
     bool cwait;
 
@@ -126,25 +130,35 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
             ++cur;
         }
         const int cnt = r_left < kCH ? r_left : kCH;
-        uint8_t* sbase = ring + slot * slotB;
-        clen = (clen & ~(0xffu << (8 * slot))) | ((unsigned)cnt << (8 * slot));
-        if (this->lane == 0) mbar_expect_tx(&mbar[slot], (unsigned)(cnt * SREC));
+        const unsigned sbase = ring + slot * slotB;
+        const unsigned bar = mbar + 8 * slot;
+        // slot holds the chunk's records at stride SREC in ascending node order;
+        // bit 7 of the chunk's byte marks a descending run
+        const unsigned long long rev = (!VERT && r_dir < 0) ? 0x80ull : 0ull;
+        clen = (clen & ~(0xffull << (8 * slot))) | (((unsigned long long)cnt | rev) << (8 * slot));
+        if (this->lane == 0) mbar_expect_tx_s(bar, (unsigned)(cnt * SREC));
         __syncwarp();
         fence_proxy_async();     // the slot was read through the generic proxy
         __syncwarp();
-        if (this->lane < cnt) {
+        if constexpr (!VERT) {   // H: the chunk's records are contiguous -> one bulk copy
+            if (this->lane == 0) {
+                const int first = r_dir > 0 ? r_start : r_start - cnt + 1;
+                tma_load_s(sbase, this->src + (size_t)this->q_of(first) * SREC, cnt * SREC, bar);
+            }
+        } else if (this->lane < cnt) {
             const size_t q = (size_t)this->q_of(r_start + r_dir * this->lane);
-            tma_load(sbase + this->lane * REC, this->src + q * SREC, SREC, &mbar[slot]);
+            tma_load_s(sbase + this->lane * SREC, this->src + q * SREC, SREC, bar);
         }
         r_start += r_dir * cnt;
         r_left -= cnt;
     }
-    __device__ __forceinline__ void ring_init(char* wsm, const RingShared& lay) {
-        ring = reinterpret_cast<uint8_t*>(wsm + lay.ring);
-        mbar = reinterpret_cast<uint64_t*>(wsm + lay.mbar);
+    __device__ __forceinline__ void ring_init(char* wsm, const RingShared<kCH, kNSlot>& lay) {
+        ring = smem_addr(wsm + lay.ring);
+        mbar = smem_addr(wsm + lay.mbar);
         slotB = lay.slot;
         if (this->lane == 0) {
-            for (int k = 0; k < kNSlot; ++k) mbar_init(&mbar[k], 1);
+            uint64_t* b = reinterpret_cast<uint64_t*>(wsm + lay.mbar);
+            for (int k = 0; k < kNSlot; ++k) mbar_init(&b[k], 1);
             fence_mbar_init();
         }
         __syncwarp();
@@ -158,14 +172,16 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
     }
     __device__ __forceinline__ void pop(int (&F)[LPL]) {
         if (cwait) {
-            mbar_wait(&mbar[cslot], (cphase >> cslot) & 1u);
+            mbar_wait_s(mbar + 8 * cslot, (cphase >> cslot) & 1u);
             __syncwarp();
             cphase ^= 1u << cslot;
-            ccount = (int)((clen >> (8 * cslot)) & 0xffu);
+            const unsigned b = (unsigned)((clen >> (8 * cslot)) & 0xffull);
+            ccount = (int)(b & 0x7fu);
+            crev = (b & 0x80u) != 0;
             cidx = 0;
             cwait = false;
         }
-        this->dec(ring + cslot * slotB + cidx * REC, F);
+        this->dec(ring + cslot * slotB + (crev ? ccount - 1 - cidx : cidx) * SREC, F);
         if (++cidx == ccount) {
             __syncwarp();
             fill(cslot);
@@ -179,12 +195,13 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         if (len0 < 2) return;
         int kk = (31 - __clz(len0)) - 1;          // spine: nodes lo + (len0 >> k) - 1
         int target = len0 >> kk;
+        int F[LPL];
+        pop(F);
 #pragma unroll 1
         for (int p = lo; p < end; ++p) {
-            int F[LPL];
-            pop(F);
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi[e] += F[e];
+            if (p + 1 < end) pop(F);     // next node's record decodes while this Msg runs
             this->msg_(phi);
             if (p + 2 - lo == target) {
                 st_i32<LPL>(this->P.fwd + this->moff(p + 1), phi);
@@ -198,12 +215,13 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         if (lenB < 2) return;
         int kk = 31 - __clz(lenB - 1);            // spine: nodes hi - ceil(lenB/2^k) + 1
         int target = ((lenB - 1) >> kk) + 1;
+        int F[LPL];
+        pop(F);
 #pragma unroll 1
         for (int p = hi; p > end; --p) {
-            int F[LPL];
-            pop(F);
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi[e] += F[e];
+            if (p - 1 > end) pop(F);     // next node's record decodes while this Msg runs
             this->msg_(phi);
             if (hi - p + 2 == target) {
                 st_i32<LPL>(this->P.bwd + this->moff(p - 1), phi);
@@ -226,13 +244,13 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
 
 // Level 0: the whole chain [0, n-1] with zero boundary messages; warp 0 runs the
 // forward pass into i, warp 1 the backward pass into j, warp 0 the Handshake.
-template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
 __global__ void __launch_bounds__(64) hm_root_kernel(PassArgs a) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
-    const RingShared lay(KP);
-    Task<LPL, VERT, PAD, WIN, FIRST> h;
+    const RingShared<kRootCH, kRootNS> lay(KP);
+    Task<LPL, VERT, PAD, WIN, FIRST, kRootCH, kRootNS> h;
     h.init(a, blockIdx.x, lane);
     h.ring_init(smem + warp * lay.total, lay);
     const int n = h.n, i = n / 2 - 1, j = i + 1;
@@ -261,13 +279,13 @@ __global__ void __launch_bounds__(64) hm_root_kernel(PassArgs a) {
 }
 
 // Level lev >= 1: one warp per (chain, subchain s) task.
-template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST, int NW>
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int NW>
 __global__ void __launch_bounds__(NW * 32) hm_level_kernel(PassArgs a, int lev, int ntasks) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
-    const RingShared lay(KP);
-    Task<LPL, VERT, PAD, WIN, FIRST> h;
+    const RingShared<kLevCH, kLevNS> lay(KP);
+    Task<LPL, VERT, PAD, WIN, FIRST, kLevCH, kLevNS> h;
     h.init(a, 0, lane);
     h.ring_init(smem + warp * lay.total, lay);
     const int n = h.n;
@@ -316,7 +334,7 @@ struct LeafShared {     // per-warp shared memory (bytes)
 
 // One warp per leaf block [lo, hi] (level lstar): TMA-stage its records, D rows
 // and boundary messages, then solve its sub-hierarchy on chip, depth first.
-template <int LPL, bool VERT, bool PAD, bool WIN, bool FIRST>
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
 __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lstar, int nblocks) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -324,12 +342,14 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
     constexpr int KP = PS::KP, REC = PS::REC, SREC = PS::SREC;
     const LeafShared lay(KP);
     char* wsm = smem + warp * lay.total;
-    uint8_t* sF = reinterpret_cast<uint8_t*>(wsm + lay.F);
-    uint8_t* sD = FIRST ? sF : reinterpret_cast<uint8_t*>(wsm + lay.D);
-    const int strideD = FIRST ? REC : KP;      // FIRST: the D rows are the staged records
+    const unsigned wsa = smem_addr(wsm);
+    const unsigned sF = wsa + lay.F;
+    const unsigned sD = FIRST ? sF : wsa + lay.D;
+    const int strideD = KP;                    // FIRST: the D rows are the staged records (SREC = KP)
     uint8_t* stk = reinterpret_cast<uint8_t*>(wsm + lay.stack);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(wsm + lay.mbar);
-    if (lane == 0) { mbar_init(bar, 1); fence_mbar_init(); }
+    const unsigned stka = wsa + lay.stack;
+    const unsigned bar = wsa + lay.mbar;
+    if (lane == 0) { mbar_init(reinterpret_cast<uint64_t*>(wsm + lay.mbar), 1); fence_mbar_init(); }
     __syncwarp();
     unsigned phase = 0;
     const bool last = a.last != 0;
@@ -347,20 +367,26 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
         const int m = hi0 - lo0 + 1;
         // ---- stage: records, D rows, boundary messages (one mbarrier phase)
         const unsigned bytes = m * SREC + (FIRST ? 0 : m * KP) + (lstar > 0 ? 2 * KP * 4 : 0);
-        if (lane == 0) mbar_expect_tx(bar, bytes);
+        if (lane == 0) mbar_expect_tx_s(bar, bytes);
         __syncwarp();
         fence_proxy_async();
         __syncwarp();
-        if (lane < m) {
+        if constexpr (!VERT) {   // H: the block's records and D rows are contiguous
+            if (lane == 0) {
+                const size_t q = (size_t)h.q_of(lo0);
+                tma_load_s(sF, h.src + q * SREC, m * SREC, bar);
+                if (!FIRST) tma_load_s(sD, h.P.D + q * KP, m * KP, bar);
+            }
+        } else if (lane < m) {
             const size_t q = (size_t)h.q_of(lo0 + lane);
-            tma_load(sF + lane * REC, h.src + q * SREC, SREC, bar);
-            if (!FIRST) tma_load(sD + lane * KP, h.P.D + q * KP, KP, bar);
+            tma_load_s(sF + lane * SREC, h.src + q * SREC, SREC, bar);
+            if (!FIRST) tma_load_s(sD + lane * KP, h.P.D + q * KP, KP, bar);
         }
         if (lstar > 0 && lane == 30)
-            tma_load(wsm + lay.L, h.P.fwd + (size_t)h.q_of(lo0) * KP, KP * 4, bar);
+            tma_load_s(wsa + lay.L, h.P.fwd + (size_t)h.q_of(lo0) * KP, KP * 4, bar);
         if (lstar > 0 && lane == 31)
-            tma_load(wsm + lay.R, h.P.bwd + (size_t)h.q_of(hi0) * KP, KP * 4, bar);
-        mbar_wait(bar, phase);
+            tma_load_s(wsa + lay.R, h.P.bwd + (size_t)h.q_of(hi0) * KP, KP * 4, bar);
+        mbar_wait_s(bar, phase);
         __syncwarp();
         phase ^= 1u;
         int L[LPL], R[LPL];
@@ -378,8 +404,8 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
         while (true) {
             if (lo == hi) {
                 int F[LPL], Dv[LPL], lam[LPL], o[LPL];
-                h.dec(sF + lo * REC, F);
-                ld_u8<LPL>(sD + lo * strideD + lane * LPL, Dv);
+                h.dec(sF + lo * SREC, F);
+                ld_u8_s<LPL>(sD + lo * strideD + lane * LPL, Dv);
                 int lmin = INT_MAX;
 #pragma unroll
                 for (int e = 0; e < LPL; ++e) {
@@ -408,8 +434,8 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
                 lo = (int)((stkJ >> (4 * sp)) & 0xfu);
                 hi = sp == 0 ? m - 1 : (int)((stkJ >> (4 * (sp - 1))) & 0xfu) - 1;
                 __syncwarp();   // record bases were written by lane 0
-                ld_rec<LPL>(stk + (2 * sp) * REC, lane, L);
-                ld_rec<LPL>(stk + (2 * sp + 1) * REC, lane, R);
+                ld_rec_s<LPL>(stka + (2 * sp) * REC, lane, L);
+                ld_rec_s<LPL>(stka + (2 * sp + 1) * REC, lane, R);
                 continue;
             }
             const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
@@ -421,22 +447,22 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
             for (int s = 0; s < nf || s < nb; ++s) {
                 if (s < nf) {
                     int F[LPL];
-                    h.dec(sF + (lo + s) * REC, F);
+                    h.dec(sF + (lo + s) * SREC, F);
 #pragma unroll
                     for (int e = 0; e < LPL; ++e) pl[e] += F[e];
                     h.msg_(pl);
                 }
                 if (s < nb) {
                     int F[LPL];
-                    h.dec(sF + (hi - s) * REC, F);
+                    h.dec(sF + (hi - s) * SREC, F);
 #pragma unroll
                     for (int e = 0; e < LPL; ++e) pr[e] += F[e];
                     h.msg_(pr);
                 }
             }
             int Fi[LPL], Fj[LPL];
-            h.dec(sF + i * REC, Fi);
-            h.dec(sF + j * REC, Fj);
+            h.dec(sF + i * SREC, Fi);
+            h.dec(sF + j * SREC, Fj);
             handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, h.ws, h.wsT, lane, h.K);
             // push the right piece (j, hi, phi_ij, R); continue with (lo, i, L, phi_ji')
             stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
@@ -462,7 +488,7 @@ static int leaf_level(int n) {
     return l;
 }
 
-template <int LPL, bool PAD, bool WIN, bool FIRST, bool VERT>
+template <int LPL, bool PAD, int WIN, bool FIRST, bool VERT>
 static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     constexpr int KP = 32 * LPL;
     const int chains = VERT ? a.L.W : a.L.H;
@@ -472,10 +498,11 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (lstar > 0) {
-        const int rs = RingShared(KP).total;
+        const int rr = RingShared<kRootCH, kRootNS>(KP).total;
         auto rk = hm_root_kernel<LPL, VERT, PAD, WIN, FIRST>;
-        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * rs);
-        rk<<<dim3(chains, nframes), 64, 2 * rs, s>>>(a);
+        cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * rr);
+        rk<<<dim3(chains, nframes), 64, 2 * rr, s>>>(a);
+        const int rs = RingShared<kLevCH, kLevNS>(KP).total;
         auto lk = hm_level_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
         cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNWG * rs);
         int per_sm = 0;
@@ -500,24 +527,28 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     kern<<<dim3(grid, nframes), kNWL * 32, smem, s>>>(a, lstar, nblocks);
 }
 
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 static void launch_dir(const PassArgs& a, int vertical, int nframes, cudaStream_t s) {
     if (vertical) launch_cfg<LPL, PAD, WIN, false, true>(a, nframes, s);
     else if (a.first) launch_cfg<LPL, PAD, WIN, true, false>(a, nframes, s);
     else launch_cfg<LPL, PAD, WIN, false, false>(a, nframes, s);
 }
 
+template <int LPL, bool PAD>
+static void launch_win(const PassArgs& a, int vertical, int nframes, cudaStream_t s) {
+    if (a.T > LPL + 1) launch_dir<LPL, PAD, 0>(a, vertical, nframes, s);
+    else if constexpr (LPL >= 4) {
+        if (a.T == 4) launch_dir<LPL, PAD, 4>(a, vertical, nframes, s);   // the default T
+        else launch_dir<LPL, PAD, -1>(a, vertical, nframes, s);
+    } else {
+        launch_dir<LPL, PAD, -1>(a, vertical, nframes, s);
+    }
+}
+
 template <int LPL>
 static void launch_lpl(const PassArgs& a, int vertical, int nframes, cudaStream_t s) {
-    const bool pad = a.L.K != 32 * LPL;
-    const bool win = a.T <= LPL + 1;
-    if (pad) {
-        if (win) launch_dir<LPL, true, true>(a, vertical, nframes, s);
-        else launch_dir<LPL, true, false>(a, vertical, nframes, s);
-    } else {
-        if (win) launch_dir<LPL, false, true>(a, vertical, nframes, s);
-        else launch_dir<LPL, false, false>(a, vertical, nframes, s);
-    }
+    if (a.L.K != 32 * LPL) launch_win<LPL, true>(a, vertical, nframes, s);
+    else launch_win<LPL, false>(a, vertical, nframes, s);
 }
 
 int hm_launches_per_pass(const PassArgs& a, int vertical, int /*wave*/) {

@@ -71,6 +71,81 @@ __device__ __forceinline__ void st_u8(uint8_t* p, const int (&v)[LPL]) {
     }
 }
 
+// ---- explicit shared-memory loads on 32-bit shared addresses (keeps the
+// generic->shared window conversion out of the inner loops)
+__device__ __forceinline__ unsigned lds32(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint2 lds64(unsigned a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128(unsigned a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned lds16(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned lds8(unsigned a) {
+    unsigned v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
+// record at shared address `rec`: F[e] = base + v[lane*LPL + e]
+template <int LPL>
+__device__ __forceinline__ void ld_rec_s(unsigned rec, int lane, int (&F)[LPL]) {
+    constexpr int KP = 32 * LPL;
+    const int base = (int)lds32(rec + 2 * KP);
+    const unsigned p = rec + 2 * LPL * lane;
+    if constexpr (LPL == 1) {
+        F[0] = base + (int)lds16(p);
+    } else {
+        unsigned w[LPL / 2];
+        if constexpr (LPL == 2) {
+            w[0] = lds32(p);
+        } else if constexpr (LPL == 4) {
+            uint2 t = lds64(p);
+            w[0] = t.x; w[1] = t.y;
+        } else {
+            uint4 t = lds128(p);
+            w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+        }
+#pragma unroll
+        for (int q = 0; q < LPL / 2; ++q) {
+            F[2 * q] = base + (int)(w[q] & 0xffffu);
+            F[2 * q + 1] = base + (int)(w[q] >> 16);
+        }
+    }
+}
+
+// LPL bytes at shared address p (this lane's D labels)
+template <int LPL>
+__device__ __forceinline__ void ld_u8_s(unsigned p, int (&v)[LPL]) {
+    if constexpr (LPL == 1) {
+        v[0] = (int)lds8(p);
+    } else if constexpr (LPL == 2) {
+        const unsigned t = lds16(p);
+        v[0] = t & 0xff; v[1] = t >> 8;
+    } else if constexpr (LPL == 4) {
+        const unsigned t = lds32(p);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) v[b] = __byte_perm(t, 0, 0x4440 + b);
+    } else {
+        const uint2 t = lds64(p);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) { v[b] = __byte_perm(t.x, 0, 0x4440 + b); v[4 + b] = __byte_perm(t.y, 0, 0x4440 + b); }
+    }
+}
+
 // ---- compact records: u16 v[KP] | int32 base | pad  (value = base + v)
 template <int LPL>
 __device__ __forceinline__ void ld_rec(const uint8_t* rec, int lane, int (&F)[LPL]) {
@@ -145,6 +220,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx_s(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -177,7 +268,11 @@ __device__ __forceinline__ int dt_op3(int a, int b, int c) {
     return MAX ? __vimax3_s32(a, b, c) : __vimin3_s32(a, b, c);
 }
 
-template <int LPL, bool PAD, bool WIN, bool MAX = false>
+// WIN: 0 = full Kogge-Stone scan across lanes (any T); -1 = one-hop window,
+// runtime T <= LPL+1; > 0 = one-hop window with compile-time T == WIN, so the
+// candidates that are provably >= the truncation term (left-lane candidates of
+// labels e with e+1 >= T, right-lane ones with LPL-e >= T) are never formed.
+template <int LPL, bool PAD, int WIN, bool MAX = false>
 __device__ __forceinline__ void dtrans(int (&x)[LPL], int ws_, int wsT_, int lane, int K) {
     const int big = MAX ? -kBig : kBig;
     const int ws = MAX ? -ws_ : ws_;
@@ -199,7 +294,7 @@ __device__ __forceinline__ void dtrans(int (&x)[LPL], int ws_, int wsT_, int lan
 #pragma unroll
     for (int e = LPL - 2; e >= 0; --e) bw[e] = dt_addop<MAX>(bw[e + 1], ws, x[e]);
     int inf, inb;
-    if constexpr (WIN) {
+    if constexpr (WIN != 0) {
         inf = __shfl_up_sync(kFull, fw[LPL - 1], 1);
         inb = __shfl_down_sync(kFull, bw[0], 1);
     } else {
@@ -219,14 +314,16 @@ __device__ __forceinline__ void dtrans(int (&x)[LPL], int ws_, int wsT_, int lan
     if (lane == 31) inb = big;
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
-        const int vf = dt_addop<MAX>(inf, ws * (e + 1), fw[e]);
-        const int vb = dt_addop<MAX>(inb, ws * (LPL - e), bw[e]);
+        const bool needL = WIN > 0 ? (e + 1 < WIN) : true;
+        const bool needR = WIN > 0 ? (LPL - e < WIN) : true;
+        const int vf = needL ? dt_addop<MAX>(inf, ws * (e + 1), fw[e]) : fw[e];
+        const int vb = needR ? dt_addop<MAX>(inb, ws * (LPL - e), bw[e]) : bw[e];
         x[e] = dt_op3<MAX>(vf, vb, cap);
     }
 }
 
 // out(b) = min_a x(a) + ws*min(|a-b|, T), in place, exact (Msg).
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 __device__ __forceinline__ void msg(int (&x)[LPL], int ws, int wsT, int lane, int K) {
     dtrans<LPL, PAD, WIN, false>(x, ws, wsT, lane, K);
 }
@@ -234,7 +331,7 @@ __device__ __forceinline__ void msg(int (&x)[LPL], int ws, int wsT, int lane, in
 // Handshake (Alg.5, readings R9/R10) on register vectors.
 // In: pl = message into i from the left, pr = message into j from the right,
 // Fi, Fj = node costs.  Out: pl = phi_ij (into j), pr = phi_ji' (into i).
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 __device__ __forceinline__ void handshake_regs(const int (&Fi)[LPL], const int (&Fj)[LPL], int (&pl)[LPL],
                                                int (&pr)[LPL], int ws, int wsT, int lane, int K) {
     int pji[LPL], t_[LPL];

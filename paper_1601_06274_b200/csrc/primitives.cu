@@ -23,7 +23,7 @@ __device__ __forceinline__ void st_dense(int32_t* p, int K, int lane, const int 
     }
 }
 
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 __global__ void msg_batch_kernel(const int32_t* a, int32_t* out, int count, int K, int ws, int wsT) {
     const int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (v >= count) return;
@@ -33,7 +33,7 @@ __global__ void msg_batch_kernel(const int32_t* a, int32_t* out, int count, int 
     st_dense<LPL>(out + (size_t)v * K, K, lane, x);
 }
 
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 __global__ void handshake_batch_kernel(const int32_t* Fi, const int32_t* Fj, const int32_t* pL,
                                        const int32_t* pR, int32_t* oij, int32_t* oji, int count, int K, int ws,
                                        int wsT) {
@@ -50,7 +50,7 @@ __global__ void handshake_batch_kernel(const int32_t* Fi, const int32_t* Fj, con
     st_dense<LPL>(oji + o, K, lane, pr);
 }
 
-template <int LPL, bool PAD, bool WIN>
+template <int LPL, bool PAD, int WIN>
 static void launch_prim(bool hs, const int32_t* a0, const int32_t* a1, const int32_t* a2, const int32_t* a3,
                         int32_t* o0, int32_t* o1, int count, int K, int ws, int wsT, cudaStream_t s) {
     const int grid = (count + 3) / 4;
@@ -63,12 +63,14 @@ static void launch_prim(bool hs, const int32_t* a0, const int32_t* a1, const int
 template <int LPL>
 static void dispatch(bool hs, const int32_t* a0, const int32_t* a1, const int32_t* a2, const int32_t* a3,
                      int32_t* o0, int32_t* o1, int count, int K, int ws, int T, cudaStream_t s) {
-    const bool pad = K != 32 * LPL, win = T <= LPL + 1;
+    const bool pad = K != 32 * LPL, win = T <= LPL + 1, t4 = LPL >= 4 && T == 4;
     const int wsT = ws * T;
-    if (pad && win) launch_prim<LPL, true, true>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
-    else if (pad) launch_prim<LPL, true, false>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
-    else if (win) launch_prim<LPL, false, true>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
-    else launch_prim<LPL, false, false>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    if (pad && t4) launch_prim<LPL, true, 4>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    else if (pad && win) launch_prim<LPL, true, -1>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    else if (pad) launch_prim<LPL, true, 0>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    else if (t4) launch_prim<LPL, false, 4>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    else if (win) launch_prim<LPL, false, -1>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
+    else launch_prim<LPL, false, 0>(hs, a0, a1, a2, a3, o0, o1, count, K, ws, wsT, s);
 }
 
 static dmm_status run(bool hs, const int32_t* a0, const int32_t* a1, const int32_t* a2, const int32_t* a3,
