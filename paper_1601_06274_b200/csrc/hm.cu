@@ -332,6 +332,40 @@ struct LeafShared {     // per-warp shared memory (bytes)
     }
 };
 
+// Emit leaf `node` (chain index) with boundary messages Lb, Rb, unaries F and
+// its staged D row at shared address dD: lambda = L + F + R (reading R8); the
+// output record is L + R + D*2^F; bound += min lambda; last V: label.
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
+__device__ __forceinline__ void leaf_emit(const Pass<LPL, VERT, PAD, WIN, FIRST>& h, unsigned dD, int node,
+                                          const int (&Lb)[LPL], const int (&Rb)[LPL], const int (&F)[LPL],
+                                          bool last, long long& bsum) {
+    constexpr int REC = Pass<LPL, VERT, PAD, WIN, FIRST>::REC;
+    const int lane = h.lane;
+    int Dv[LPL], lam[LPL], o[LPL];
+    ld_u8_s<LPL>(dD + lane * LPL, Dv);
+    int lmin = INT_MAX;
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) {
+        const int lr = Lb[e] + Rb[e];
+        o[e] = lr + (Dv[e] << h.fbits);
+        lam[e] = lr + F[e];
+        if (PAD && lane * LPL + e >= h.K) lam[e] = INT_MAX;
+        lmin = min(lmin, lam[e]);
+    }
+    const int q = h.q_of(node);
+    st_rec<LPL, PAD>(h.dst + (size_t)q * REC, lane, o, h.K);
+    const int gmin = __reduce_min_sync(kFull, lmin);
+    bsum += gmin;
+    if (VERT && last) {
+        int kmin = INT_MAX;
+#pragma unroll
+        for (int e = LPL - 1; e >= 0; --e)
+            if (lam[e] == gmin) kmin = lane * LPL + e;
+        kmin = __reduce_min_sync(kFull, kmin);
+        if (lane == 0) h.P.labels[q] = (uint8_t)kmin;
+    }
+}
+
 // One warp per leaf block [lo, hi] (level lstar): TMA-stage its records, D rows
 // and boundary messages, then solve its sub-hierarchy on chip, depth first.
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
@@ -397,82 +431,82 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
 #pragma unroll
             for (int e = 0; e < LPL; ++e) { L[e] = 0; R[e] = 0; }
         }
-        // ---- the block's sub-hierarchy, depth first
+        // ---- the block's sub-hierarchy, depth first.  A child of length 1 is
+        // emitted right after its parent's Handshake (its F is in registers) and
+        // the walk continues with the sibling, so only pieces whose children
+        // are both longer than one node push to the stack.
         int lo = 0, hi = m - 1, sp = 0;
-        unsigned stkJ = 0;
+        unsigned stkJ = 0, stkH = 0;   // pending pieces [j_k, hi_k], 4 bits each, per-lane registers
 #pragma unroll 1
         while (true) {
-            if (lo == hi) {
-                int F[LPL], Dv[LPL], lam[LPL], o[LPL];
+            bool done_piece = false;
+            if (lo == hi) {                       // a one-node block
+                int F[LPL];
                 h.dec(sF + lo * SREC, F);
-                ld_u8_s<LPL>(sD + lo * strideD + lane * LPL, Dv);
-                int lmin = INT_MAX;
+                leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, sD + lo * strideD, lo0 + lo, L, R, F, last, bsum);
+                done_piece = true;
+            } else {
+                const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
+                int pl[LPL], pr[LPL];
 #pragma unroll
-                for (int e = 0; e < LPL; ++e) {
-                    const int lr = L[e] + R[e];
-                    o[e] = lr + (Dv[e] << h.fbits);
-                    lam[e] = lr + F[e];
-                    if (PAD && lane * LPL + e >= h.K) lam[e] = INT_MAX;
-                    lmin = min(lmin, lam[e]);
-                }
-                const int node = lo0 + lo;
-                st_rec<LPL, PAD>(h.dst + (size_t)h.q_of(node) * REC, lane, o, h.K);
-                const int gmin = __reduce_min_sync(kFull, lmin);
-                bsum += gmin;
-                if (VERT && last) {
-                    int kmin = INT_MAX;
+                for (int e = 0; e < LPL; ++e) { pl[e] = L[e]; pr[e] = R[e]; }
+                const int nf = i - lo, nb = hi - j;
+#pragma unroll 1
+                for (int s = 0; s < nf || s < nb; ++s) {
+                    if (s < nf) {
+                        int F[LPL];
+                        h.dec(sF + (lo + s) * SREC, F);
 #pragma unroll
-                    for (int e = LPL - 1; e >= 0; --e)
-                        if (lam[e] == gmin) kmin = lane * LPL + e;
-                    kmin = __reduce_min_sync(kFull, kmin);
-                    if (lane == 0) h.P.labels[h.q_of(node)] = (uint8_t)kmin;
+                        for (int e = 0; e < LPL; ++e) pl[e] += F[e];
+                        h.msg_(pl);
+                    }
+                    if (s < nb) {
+                        int F[LPL];
+                        h.dec(sF + (hi - s) * SREC, F);
+#pragma unroll
+                        for (int e = 0; e < LPL; ++e) pr[e] += F[e];
+                        h.msg_(pr);
+                    }
                 }
+                int Fi[LPL], Fj[LPL];
+                h.dec(sF + i * SREC, Fi);
+                h.dec(sF + j * SREC, Fj);
+                handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, h.ws, h.wsT, lane, h.K);
+                // children: A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R)
+                const bool leafA = (i == lo), leafB = (j == hi);
+                if (leafA) leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, sD + i * strideD, lo0 + i, L, pr, Fi, last, bsum);
+                if (leafB) leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, sD + j * strideD, lo0 + j, pl, R, Fj, last, bsum);
+                if (leafA && leafB) {
+                    done_piece = true;
+                } else if (leafA) {                 // continue with B
+                    lo = j;
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) L[e] = pl[e];
+                } else if (leafB) {                 // continue with A
+                    hi = i;
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) R[e] = pr[e];
+                } else {                            // push B, continue with A
+                    stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
+                    stkH = (stkH & ~(0xfu << (4 * sp))) | ((unsigned)hi << (4 * sp));
+                    __syncwarp();   // every lane has read this stack slot's previous bases
+                    st_rec<LPL, false>(stk + (2 * sp) * REC, lane, pl, h.K);
+                    st_rec<LPL, false>(stk + (2 * sp + 1) * REC, lane, R, h.K);
+                    ++sp;
+                    hi = i;
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) R[e] = pr[e];
+                }
+            }
+            if (done_piece) {
                 if (sp == 0) break;
                 --sp;
-                // pending piece k = [j_k, hi_k], hi_0 = m-1, hi_k = j_{k-1} - 1:
-                // the j's are a per-lane register (4 bits each)
                 lo = (int)((stkJ >> (4 * sp)) & 0xfu);
-                hi = sp == 0 ? m - 1 : (int)((stkJ >> (4 * (sp - 1))) & 0xfu) - 1;
+                hi = (int)((stkH >> (4 * sp)) & 0xfu);
                 __syncwarp();   // record bases were written by lane 0
-                ld_rec_s<LPL>(stka + (2 * sp) * REC, lane, L);
-                ld_rec_s<LPL>(stka + (2 * sp + 1) * REC, lane, R);
-                continue;
+                ld_rec<LPL>(stk + (2 * sp) * REC, lane, L);
+                ld_rec<LPL>(stk + (2 * sp + 1) * REC, lane, R);
             }
-            const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
-            int pl[LPL], pr[LPL];
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) { pl[e] = L[e]; pr[e] = R[e]; }
-            const int nf = i - lo, nb = hi - j;
-#pragma unroll 1
-            for (int s = 0; s < nf || s < nb; ++s) {
-                if (s < nf) {
-                    int F[LPL];
-                    h.dec(sF + (lo + s) * SREC, F);
-#pragma unroll
-                    for (int e = 0; e < LPL; ++e) pl[e] += F[e];
-                    h.msg_(pl);
-                }
-                if (s < nb) {
-                    int F[LPL];
-                    h.dec(sF + (hi - s) * SREC, F);
-#pragma unroll
-                    for (int e = 0; e < LPL; ++e) pr[e] += F[e];
-                    h.msg_(pr);
-                }
-            }
-            int Fi[LPL], Fj[LPL];
-            h.dec(sF + i * SREC, Fi);
-            h.dec(sF + j * SREC, Fj);
-            handshake_regs<LPL, PAD, WIN>(Fi, Fj, pl, pr, h.ws, h.wsT, lane, h.K);
-            // push the right piece (j, hi, phi_ij, R); continue with (lo, i, L, phi_ji')
-            stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
-            __syncwarp();       // every lane has read this stack slot's previous bases
-            st_rec<LPL, false>(stk + (2 * sp) * REC, lane, pl, h.K);
-            st_rec<LPL, false>(stk + (2 * sp + 1) * REC, lane, R, h.K);
-            ++sp;
-            hi = i;
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) R[e] = pr[e];
         }
         __syncwarp();   // all lanes done with the staged block before the next fill
     }

@@ -90,8 +90,8 @@ __device__ __forceinline__ uint4 lds128(unsigned a) {
     return v;
 }
 __device__ __forceinline__ unsigned lds16(unsigned a) {
-    unsigned short v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    unsigned v;   // ld.u16 into a 32-bit register zero-extends
+    asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
     return v;
 }
 __device__ __forceinline__ unsigned lds8(unsigned a) {
