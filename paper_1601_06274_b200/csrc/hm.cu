@@ -170,64 +170,80 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         cslot = 0; cidx = 0; ccount = 0; cwait = true;
         for (int k = 0; k < kNSlot; ++k) fill(k);
     }
+    __device__ __forceinline__ void chunk_wait() {
+        mbar_wait_s(mbar + 8 * cslot, (cphase >> cslot) & 1u);
+        __syncwarp();
+        cphase ^= 1u << cslot;
+        const unsigned b = (unsigned)((clen >> (8 * cslot)) & 0xffull);
+        ccount = (int)(b & 0x7fu);
+        crev = (b & 0x80u) != 0;
+        cidx = 0;
+        cwait = false;
+    }
+    __device__ __forceinline__ void chunk_release() {
+        __syncwarp();
+        fill(cslot);
+        cslot = cslot + 1 == kNSlot ? 0 : cslot + 1;
+        cwait = true;
+    }
     __device__ __forceinline__ void pop(int (&F)[LPL]) {
-        if (cwait) {
-            mbar_wait_s(mbar + 8 * cslot, (cphase >> cslot) & 1u);
-            __syncwarp();
-            cphase ^= 1u << cslot;
-            const unsigned b = (unsigned)((clen >> (8 * cslot)) & 0xffull);
-            ccount = (int)(b & 0x7fu);
-            crev = (b & 0x80u) != 0;
-            cidx = 0;
-            cwait = false;
-        }
+        if (cwait) chunk_wait();
         this->dec(ring + cslot * slotB + (crev ? ccount - 1 - cidx : cidx) * SREC, F);
-        if (++cidx == ccount) {
-            __syncwarp();
-            fill(cslot);
-            cslot = cslot + 1 == kNSlot ? 0 : cslot + 1;
-            cwait = true;
-        }
+        if (++cidx == ccount) chunk_release();
     }
-    // ---- passes (spine messages to the fwd/bwd scratch arrays)
-    __device__ __forceinline__ void pass_fwd(int lo, int end, int (&phi)[LPL]) {
-        const int len0 = end - lo + 1;
-        if (len0 < 2) return;
-        int kk = (31 - __clz(len0)) - 1;          // spine: nodes lo + (len0 >> k) - 1
-        int target = len0 >> kk;
-        int F[LPL];
-        pop(F);
-#pragma unroll 1
-        for (int p = lo; p < end; ++p) {
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) phi[e] += F[e];
-            if (p + 1 < end) pop(F);     // next node's record decodes while this Msg runs
-            this->msg_(phi);
-            if (p + 2 - lo == target) {
-                st_i32<LPL>(this->P.fwd + this->moff(p + 1), phi);
+    // ---- passes: DIR = +1 forward from `first` (phi_{p+1} = Msg(phi_p + F_p)),
+    // DIR = -1 backward; nsteps Msgs.  Spine messages a later level needs go to
+    // the fwd/bwd scratch arrays: forward over a piece of len0 = nsteps + 1
+    // nodes, nodes first + (len0 >> k) - 1; backward, first - ceil(len0/2^k) + 1.
+    // The pass is run 0 of the task, so its chunks hold exactly its nodes; full
+    // chunks run unrolled with compile-time ring offsets.
+    template <int DIR>
+    __device__ __forceinline__ void run_pass(int first, int nsteps, int (&phi)[LPL]) {
+        if (nsteps < 1) return;
+        constexpr bool REV = !VERT && DIR < 0;   // H backward chunks are staged ascending
+        const int len0 = nsteps + 1;
+        int kk = DIR > 0 ? (31 - __clz(len0)) - 1 : 31 - __clz(len0 - 1);
+        int target = DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1);
+        int32_t* arr = DIR > 0 ? this->P.fwd : this->P.bwd;
+        auto spine = [&](int s) {
+            if (s + 2 == target) {
+                st_i32<LPL>(arr + this->moff(first + DIR * (s + 1)), phi);
                 --kk;
-                target = kk >= 0 ? (len0 >> kk) : INT_MAX;
+                target = kk < 0 ? INT_MAX : (DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1));
             }
-        }
-    }
-    __device__ __forceinline__ void pass_bwd(int hi, int end, int (&phi)[LPL]) {
-        const int lenB = hi - end + 1;
-        if (lenB < 2) return;
-        int kk = 31 - __clz(lenB - 1);            // spine: nodes hi - ceil(lenB/2^k) + 1
-        int target = ((lenB - 1) >> kk) + 1;
-        int F[LPL];
-        pop(F);
+        };
+        int s = 0;
 #pragma unroll 1
-        for (int p = hi; p > end; --p) {
+        while (s < nsteps) {
+            chunk_wait();
+            const unsigned base = ring + cslot * slotB;
+            if (ccount == kCH) {
+                int F[LPL];
+                this->dec(base + (REV ? kCH - 1 : 0) * SREC, F);
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) phi[e] += F[e];
-            if (p - 1 > end) pop(F);     // next node's record decodes while this Msg runs
-            this->msg_(phi);
-            if (hi - p + 2 == target) {
-                st_i32<LPL>(this->P.bwd + this->moff(p - 1), phi);
-                --kk;
-                target = kk >= 0 ? (((lenB - 1) >> kk) + 1) : INT_MAX;
+                for (int k = 0; k < kCH; ++k) {
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) phi[e] += F[e];
+                    if (k + 1 < kCH) this->dec(base + (REV ? kCH - 2 - k : k + 1) * SREC, F);
+                    this->msg_(phi);
+                    spine(s + k);
+                }
+                s += kCH;
+            } else {
+                const int cnt = ccount;
+                int F[LPL];
+                this->dec(base + (REV ? cnt - 1 : 0) * SREC, F);
+#pragma unroll 1
+                for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) phi[e] += F[e];
+                    if (k + 1 < cnt) this->dec(base + (REV ? cnt - 2 - k : k + 1) * SREC, F);
+                    this->msg_(phi);
+                    spine(s + k);
+                }
+                s += cnt;
             }
+            chunk_release();
         }
     }
     // Handshake (Alg.5); the ring delivers F_j then F_i.  Writes the
@@ -262,12 +278,12 @@ __global__ void __launch_bounds__(64) hm_root_kernel(PassArgs a) {
         h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
         h.start(2);
         st_i32<LPL>(h.P.fwd + h.moff(0), zero);
-        h.pass_fwd(0, i, phi);
+        h.template run_pass<1>(0, i, phi);
     } else {
         h.rs0 = n - 1; h.rd0 = -1; h.rc0 = n - 1 - j;
         h.start(1);
         st_i32<LPL>(h.P.bwd + h.moff(n - 1), zero);
-        h.pass_bwd(n - 1, j, phi);
+        h.template run_pass<-1>(n - 1, n - 1 - j, phi);
         st_i32<LPL>(h.P.bwd + h.moff(j), phi);
     }
     __syncthreads();
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(NW * 32) hm_level_kernel(PassArgs a, int lev, 
             h.start(2);
             ld_i32<LPL>(h.P.bwd + h.moff(hi), bnd);
             ld_i32<LPL>(h.P.fwd + h.moff(ii), spn);
-            h.pass_bwd(hi, j, bnd);
+            h.template run_pass<-1>(hi, hi - j, bnd);
             h.handshake(ii, spn, bnd);
         } else {          // right piece: right boundary kept -> reuse bwd, recompute fwd
             h.rs0 = lo; h.rd0 = 1; h.rc0 = ii - lo;
@@ -311,7 +327,7 @@ __global__ void __launch_bounds__(NW * 32) hm_level_kernel(PassArgs a, int lev, 
             h.start(2);
             ld_i32<LPL>(h.P.fwd + h.moff(lo), bnd);
             ld_i32<LPL>(h.P.bwd + h.moff(j), spn);
-            h.pass_fwd(lo, ii, bnd);
+            h.template run_pass<1>(lo, ii - lo, bnd);
             h.handshake(ii, bnd, spn);
         }
     }
@@ -381,7 +397,6 @@ __global__ void __launch_bounds__(kNWL * 32) hm_leaf_kernel(PassArgs a, int lsta
     const unsigned sD = FIRST ? sF : wsa + lay.D;
     const int strideD = KP;                    // FIRST: the D rows are the staged records (SREC = KP)
     uint8_t* stk = reinterpret_cast<uint8_t*>(wsm + lay.stack);
-    const unsigned stka = wsa + lay.stack;
     const unsigned bar = wsa + lay.mbar;
     if (lane == 0) { mbar_init(reinterpret_cast<uint64_t*>(wsm + lay.mbar), 1); fence_mbar_init(); }
     __syncwarp();
