@@ -191,6 +191,14 @@ DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches)
 /* Debug: value != 0 makes dmm_solve stop after the first H half-step (the
  * bound history then holds only b_0; for parity taps of f_ after H_1). */
 #define DMM_TUNE_DEBUG_STOP_AFTER_H 2
+/* DMM_TUNE_PAIR: value != 0 (default) runs the half-steps on chain pairs in
+ * packed 16-bit arithmetic (two chains per warp) whenever the configuration
+ * passes the 16-bit range check (3*w*2^F*min(T,K) + span bound + 4 <= 16383;
+ * exact, identical results); 0 forces the one-chain int32 kernels. */
+#define DMM_TUNE_PAIR 3
+/* DMM_TUNE_QUERY_PAIR: sets dmm_last_error() to "pair" or "int32", the
+ * kernel family the next half-step will use (value ignored). */
+#define DMM_TUNE_QUERY_PAIR 4
 DMM_API dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value);
 
 DMM_API const char* dmm_status_str(dmm_status s);

@@ -30,6 +30,8 @@ EXPORTS = (
 )
 BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
 TUNE_WAVE_BYTES = 1
+TUNE_PAIR = 3
+TUNE_QUERY_PAIR = 4
 PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
 
 
@@ -197,6 +199,16 @@ class Context:
     def set_wave_bytes(self, nbytes: int):
         """L2 wave budget of the chain-DP launches (0 = one launch per half-step)."""
         self._call("dmm_set_tuning", TUNE_WAVE_BYTES, int(nbytes))
+
+    def set_pair(self, enable: bool = True):
+        """Chain-pair packed 16-bit kernels (default on; used only when the
+        configuration passes the 16-bit range check) or the int32 kernels."""
+        self._call("dmm_set_tuning", TUNE_PAIR, 1 if enable else 0)
+
+    def kernel_family(self) -> str:
+        """'pair' or 'int32': the half-step kernels the next solve runs."""
+        self._call("dmm_set_tuning", TUNE_QUERY_PAIR, 0)
+        return self._lib.dmm_last_error(self._h).decode()
 
     def read_profile(self):
         """{class: (total_ms, launches)} since the last read (synchronises)."""

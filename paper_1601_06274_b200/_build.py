@@ -31,15 +31,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(p) for p in _deps()):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *sources()]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    tag = f"tmp{os.getpid()}"
+    objs = [os.path.join(os.path.dirname(LIB), os.path.basename(src)[:-3] + f".{tag}.o") for src in sources()]
+    comp = [f for f in FLAGS if f != "-shared"]
+    # one nvcc per translation unit, in parallel (the chain-DP units dominate)
+    procs = [subprocess.Popen([NVCC, *comp, "-c", "-o", o, src], stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                              text=True) for src, o in zip(sources(), objs)]
+    logs, failed = [], []
+    for src, pr in zip(sources(), procs):
+        out, _ = pr.communicate()
+        logs.append(out)
+        if pr.returncode != 0:
+            failed.append(os.path.basename(src))
+    tmp = LIB + "." + tag
+    try:
+        if failed:
+            raise RuntimeError("nvcc failed (" + ", ".join(failed) + "):\n" + "".join(logs))
+        r = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     with open(os.path.join(os.path.dirname(LIB), "ptxas.log"), "w") as f:
-        f.write(r.stdout + r.stderr)
+        f.write("".join(logs))
     if verbose:
-        print(r.stdout + r.stderr)
+        print("".join(logs))
     os.replace(tmp, LIB)
     return LIB
 

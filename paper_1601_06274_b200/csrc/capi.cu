@@ -25,6 +25,8 @@ struct dmm_ctx {
     int profiling;
     size_t wave_budget;   // bytes of chain data per launch wave (L2 sizing), 0 = one wave
     int stop_after_h;     // debug: dmm_solve runs only the first H half-step
+    int pair_ok;          // configuration passes pair_range_ok
+    int use_pair;         // DMM_TUNE_PAIR (default 1): packed chain-pair kernels when pair_ok
     struct Rec { int cls; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
@@ -58,6 +60,19 @@ long long span_bound(const dmm_config* c) {
     return (2 * w * T + maxD) << c->frac_bits;
 }
 
+// Range check of the packed chain-pair kernels (hm2.cu, hm2_device.cuh): with
+// wsT = w*2^F*min(T, K) and S = span_bound, every packed operand lies in
+// [-wsT - 1, 2*wsT + S + 2] and every distance-transform addend is clamped to
+// wsT + 1, so 3*wsT + S + 4 <= 16383 (the packed "infinity") keeps all
+// values and candidates exact in signed 16 bits.
+bool pair_range_ok(const dmm_config* c) {
+    const long long K = c->d_max - c->d_min + 1;
+    const long long w = c->w_h > c->w_v ? c->w_h : c->w_v;
+    const long long T = c->trunc < K ? c->trunc : K;
+    const long long wsT = (w << c->frac_bits) * T;
+    return 3 * wsT + span_bound(c) + 4 <= 16383;
+}
+
 int kp_of(int K) {
     int lpl = 1;
     while (32 * lpl < K) lpl *= 2;
@@ -79,6 +94,8 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->fh = (uint8_t*)take(px * (size_t)dmm::rec_bytes((int)KP));
     off->fwd = (int32_t*)take(4 * cells);
     off->bwd = (int32_t*)take(4 * cells);
+    off->fwdo = (int32_t*)take(8 * px);
+    off->bwdo = (int32_t*)take(8 * px);
     off->labels = (uint8_t*)take(px);
     off->bounds = (long long*)take(8 * 2 * (size_t)c->max_iters);
     off->energy = (long long*)take(8);
@@ -148,6 +165,11 @@ void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterati
         const size_t nw = (per_chain * chains + ctx->wave_budget - 1) / ctx->wave_budget;
         if (nw > 1) wave = (int)((chains + nw - 1) / nw);
     }
+    if (ctx->use_pair && ctx->pair_ok) {
+        Timed tm(ctx, 2 + v, s, dmm::hm2_launches_per_pass(a, v));
+        dmm::launch_hm2_pass(a, v, nframes, s);
+        return;
+    }
     Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
     dmm::launch_hm_pass(a, v, nframes, wave, s);
 }
@@ -188,6 +210,8 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.fh = (uint8_t*)(b + (size_t)off.fh);
     c->L.base.fwd = (int32_t*)(b + (size_t)off.fwd);
     c->L.base.bwd = (int32_t*)(b + (size_t)off.bwd);
+    c->L.base.fwdo = (int32_t*)(b + (size_t)off.fwdo);
+    c->L.base.bwdo = (int32_t*)(b + (size_t)off.bwdo);
     c->L.base.labels = (uint8_t*)(b + (size_t)off.labels);
     c->L.base.bounds = (long long*)(b + (size_t)off.bounds);
     c->L.base.energy = (long long*)(b + (size_t)off.energy);
@@ -200,6 +224,8 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->profiling = 0;
     c->wave_budget = 0;
     c->stop_after_h = 0;
+    c->pair_ok = pair_range_ok(cfg);
+    c->use_pair = 1;
     if (cudaSetDevice(device) != cudaSuccess) {
         dmm_destroy(c);
         return DMM_E_CUDA;
@@ -440,6 +466,8 @@ dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value) {
     if (!ctx) return DMM_E_ARG;
     if (param == DMM_TUNE_WAVE_BYTES && value >= 0) { ctx->wave_budget = (size_t)value; return DMM_OK; }
     if (param == DMM_TUNE_DEBUG_STOP_AFTER_H) { ctx->stop_after_h = value != 0; return DMM_OK; }
+    if (param == DMM_TUNE_PAIR) { ctx->use_pair = value != 0; return DMM_OK; }
+    if (param == DMM_TUNE_QUERY_PAIR) { ctx->err = ctx->use_pair && ctx->pair_ok ? "pair" : "int32"; return DMM_OK; }
     ctx->err = "unknown tuning parameter";
     return DMM_E_ARG;
 }

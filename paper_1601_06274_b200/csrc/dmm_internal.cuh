@@ -8,6 +8,7 @@
 //   fh     rec [H][W]           D*2^F + g_ (the H pass's unaries), g_ = minorant of the V pass
 //   fwd    i32 [H][W][KP]       message scratch: message into a node from the left / top
 //   bwd    i32 [H][W][KP]       message scratch: message into a node from the right / bottom
+//   fwdo, bwdo i32 [H][W][2]    pair path: per-chain offsets of the packed scratch messages
 //   labels u8  [H][W]
 // rec = compact lossless K-vector record of REC = 2*KP + 16 bytes:
 //   u16 v[KP] | int32 base | 12 B pad,  value(k) = base + v[k], base = min_k.
@@ -36,6 +37,8 @@ struct FramePtrs {
     uint8_t* fh;
     int32_t* fwd;
     int32_t* bwd;
+    int32_t* fwdo;       // pair path: the two chain offsets of a packed fwd / bwd message [H][W][2]
+    int32_t* bwdo;
     uint8_t* labels;
     long long* bounds;   // [2 * max_iters]
     long long* energy;   // [1]
@@ -61,6 +64,8 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.fh += o;
     p.fwd = (int32_t*)((char*)p.fwd + o);
     p.bwd = (int32_t*)((char*)p.bwd + o);
+    p.fwdo = (int32_t*)((char*)p.fwdo + o);
+    p.bwdo = (int32_t*)((char*)p.bwdo + o);
     p.labels += o;
     p.bounds = (long long*)((char*)p.bounds + o);
     p.energy = (long long*)((char*)p.energy + o);
@@ -88,6 +93,10 @@ void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, c
 // hm_launches_per_pass() kernels.
 void launch_hm_pass(const PassArgs& a, int vertical, int nframes, int wave, cudaStream_t s);
 int hm_launches_per_pass(const PassArgs& a, int vertical, int wave);
+// The same half-step on chain pairs in packed 16-bit arithmetic (hm2.cu);
+// valid when the configuration passes the pair range check (capi.cu).
+void launch_hm2_pass(const PassArgs& a, int vertical, int nframes, cudaStream_t s);
+int hm2_launches_per_pass(const PassArgs& a, int vertical);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);

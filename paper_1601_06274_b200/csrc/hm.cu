@@ -103,8 +103,8 @@ struct RingShared {     // per-warp shared memory (bytes): NS chunks of CH recor
 };
 // ring geometry: the root's two passes per chain are the latency-critical path
 // with few warps per SM, so they prefetch deepest (64 nodes)
-constexpr int kRootCH = 8, kRootNS = 8;
-constexpr int kLevCH = 4, kLevNS = 8;
+constexpr int kRootCH = 16, kRootNS = 4;
+constexpr int kLevCH = 8, kLevNS = 4;
 
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int kCH, int kNSlot>
 struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
@@ -537,42 +537,54 @@ static int leaf_level(int n) {
     return l;
 }
 
+// Per-instantiation launch constants (SM count, occupancy, smem opt-in),
+// queried once per device: host API calls between the ~8 launches of a
+// half-step would otherwise starve the GPU.
+struct LaunchCache {
+    int dev = -1, sms = 148, lev_cap = 148, leaf_cap = 148;
+};
+
 template <int LPL, bool PAD, int WIN, bool FIRST, bool VERT>
 static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     constexpr int KP = 32 * LPL;
-    const int chains = VERT ? a.L.W : a.L.H;
+        const int chains = VERT ? a.L.W : a.L.H;
+    const int units = chains;
     const int n = VERT ? a.L.H : a.L.W;
     const int lstar = leaf_level(n);
-    int dev = 0, sms = 148;
+    const int rr = RingShared<kRootCH, kRootNS>(KP).total;
+    const int rs = RingShared<kLevCH, kLevNS>(KP).total;
+    const int smem = kNWL * LeafShared(KP).total;
+    auto rk = hm_root_kernel<LPL, VERT, PAD, WIN, FIRST>;
+    auto lk = hm_level_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
+    auto kern = hm_leaf_kernel<LPL, VERT, PAD, WIN, FIRST>;
+    static LaunchCache lc;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (lstar > 0) {
-        const int rr = RingShared<kRootCH, kRootNS>(KP).total;
-        auto rk = hm_root_kernel<LPL, VERT, PAD, WIN, FIRST>;
+    if (lc.dev != dev) {
+        cudaDeviceGetAttribute(&lc.sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * rr);
-        rk<<<dim3(chains, nframes), 64, 2 * rr, s>>>(a);
-        const int rs = RingShared<kLevCH, kLevNS>(KP).total;
-        auto lk = hm_level_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
         cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNWG * rs);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, kNWG * 32, kNWG * rs);
-        const int cap = sms * (per_sm > 0 ? per_sm : 1);
+        lc.lev_cap = lc.sms * (per_sm > 0 ? per_sm : 1);
+        per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNWL * 32, smem);
+        lc.leaf_cap = lc.sms * (per_sm > 0 ? per_sm : 1);
+        lc.dev = dev;
+    }
+    if (lstar > 0) {
+        rk<<<dim3(units, nframes), 64, 2 * rr, s>>>(a);
         for (int lev = 1; lev < lstar; ++lev) {
-            const int ntasks = chains << lev;
+            const int ntasks = units << lev;
             int grid = (ntasks + kNWG - 1) / kNWG;
-            if (grid > cap) grid = cap;
+            if (grid > lc.lev_cap) grid = lc.lev_cap;
             lk<<<dim3(grid, nframes), kNWG * 32, kNWG * rs, s>>>(a, lev, ntasks);
         }
     }
-    const int smem = kNWL * LeafShared(KP).total;
-    auto kern = hm_leaf_kernel<LPL, VERT, PAD, WIN, FIRST>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    const int nblocks = chains << lstar;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNWL * 32, smem);
+    const int nblocks = units << lstar;
     int grid = (nblocks + kNWL - 1) / kNWL;
-    const int cap = sms * (per_sm > 0 ? per_sm : 1);
-    if (grid > cap) grid = cap;
+    if (grid > lc.leaf_cap) grid = lc.leaf_cap;
     kern<<<dim3(grid, nframes), kNWL * 32, smem, s>>>(a, lstar, nblocks);
 }
 

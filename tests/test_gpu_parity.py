@@ -17,10 +17,13 @@ def _ctx(**kw):
     return dmm.Context(**kw)
 
 
-def _run_gpu(left, right, d_min, K, w_h, w_v, T, Fb, iters, r=2, oob=-1):
+def _run_gpu(left, right, d_min, K, w_h, w_v, T, Fb, iters, r=2, oob=-1, pair=True):
     H, W = left.shape
     ctx = _ctx(width=W, height=H, d_min=d_min, d_max=d_min + K - 1, w_h=w_h, w_v=w_v, T=T,
                frac_bits=Fb, census_radius=r, oob_cost=oob, max_iters=max(iters, 1))
+    ctx.set_pair(pair)
+    if not pair:
+        assert ctx.kernel_family() == "int32"
     lt = torch.from_numpy(left).cuda()
     rt = torch.from_numpy(right).cuda()
     ctx.cost_volume(lt, rt)
@@ -84,15 +87,32 @@ CASES = [
     (2, 2, 2, 0, 9, 9, 1, 4, 3, 1, "rd"),
     (1025, 3, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),       # long rows, odd splits
     (5, 513, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),        # long columns
+    (1500, 24, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),   # C3 row length and K
 ]
 
 
+@pytest.mark.parametrize("family", ["auto", "int32"])
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}xK{c[2]}" for c in CASES])
-def test_parity_cases(orc, case):
+def test_parity_cases(orc, case, family):
+    """Both kernel families (packed chain pairs where the range check allows
+    them, and the one-chain int32 kernels) against the oracle."""
     W, H, K, d_min, w_h, w_v, T, Fb, iters, r, kind = case
     left, right, _ = datagen.pair(kind, W, H, K, seed=W * 7 + H)
     args = (d_min, K, w_h, w_v, T, Fb, iters, r)
-    _compare(_run_gpu(left, right, *args), _run_oracle(orc, left, right, *args))
+    _compare(_run_gpu(left, right, *args, pair=(family == "auto")), _run_oracle(orc, left, right, *args))
+
+
+def test_kernel_family_selection():
+    """The packed pair kernels serve the benchmark configurations; a regulariser
+    too large for 16-bit operands falls back to int32 (range check, capi.cu)."""
+    c2 = _ctx(width=64, height=8, d_min=0, d_max=127, w=3, T=4, frac_bits=4)
+    assert c2.kernel_family() == "pair"
+    c3 = _ctx(width=64, height=8, d_min=0, d_max=255, w=3, T=4, frac_bits=4)
+    assert c3.kernel_family() == "pair"
+    big = _ctx(width=64, height=8, d_min=0, d_max=99, w_h=5, w_v=2, T=7, frac_bits=8)
+    assert big.kernel_family() == "int32"
+    c2.set_pair(False)
+    assert c2.kernel_family() == "int32"
 
 
 def test_batched_frames_equal_single(orc):
