@@ -22,7 +22,7 @@ constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece st
 constexpr int kDepth = 4;    // pending right pieces in a leaf block
 template <int LPL> constexpr int nwg() { return LPL >= 8 ? 4 : 8; }   // warps per CTA, level kernels (smem)
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
-constexpr int kRootCH = 8, kRootNS = 8;
+constexpr int kRootCH = 8, kRootNS = 4;
 constexpr int kLevCH = 4, kLevNS = 4;
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
