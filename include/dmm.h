@@ -193,7 +193,7 @@ DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches)
 #define DMM_TUNE_DEBUG_STOP_AFTER_H 2
 /* DMM_TUNE_PAIR: value != 0 (default) runs the half-steps on chain pairs in
  * packed 16-bit arithmetic (two chains per warp) whenever the configuration
- * passes the 16-bit range check (3*w*2^F*min(T,K) + span bound + 4 <= 16383;
+ * passes the 16-bit range check (3*w*2^F*min(T,K) + 16*span bound + 4 <= 16383;
  * exact, identical results); 0 forces the one-chain int32 kernels. */
 #define DMM_TUNE_PAIR 3
 /* DMM_TUNE_QUERY_PAIR: sets dmm_last_error() to "pair" or "int32", the

@@ -61,16 +61,19 @@ long long span_bound(const dmm_config* c) {
 }
 
 // Range check of the packed chain-pair kernels (hm2.cu, hm2_device.cuh): with
-// wsT = w*2^F*min(T, K) and S = span_bound, every packed operand lies in
-// [-wsT - 1, 2*wsT + S + 2] and every distance-transform addend is clamped to
-// wsT + 1, so 3*wsT + S + 4 <= 16383 (the packed "infinity") keeps all
-// values and candidates exact in signed 16 bits.
+// wsT = w*2^F*min(T, K) and S = span_bound, a pass leaves its message
+// unnormalised for at most 16 steps (the ring chunk), during which its minimum
+// drifts up by <= S per step, so every packed operand lies in
+// [-wsT - 1, 16*S + wsT] and every distance-transform candidate (addends are
+// clamped to wsT + 1) below 16*S + 2*wsT + 2; 16*S + 3*wsT + 4 <= 16383 (the
+// packed "infinity", with 16383 + wsT + 1 <= 32767) keeps all values and
+// candidates exact in signed 16 bits.
 bool pair_range_ok(const dmm_config* c) {
     const long long K = c->d_max - c->d_min + 1;
     const long long w = c->w_h > c->w_v ? c->w_h : c->w_v;
     const long long T = c->trunc < K ? c->trunc : K;
     const long long wsT = (w << c->frac_bits) * T;
-    return 3 * wsT + span_bound(c) + 4 <= 16383;
+    return 16 * span_bound(c) + 3 * wsT + 4 <= 16383;
 }
 
 int kp_of(int K) {

@@ -20,10 +20,11 @@ namespace p2 {
 
 constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
 constexpr int kDepth = 4;    // pending right pieces in a leaf block
-template <int LPL> constexpr int nwg() { return LPL >= 8 ? 4 : 8; }   // warps per CTA, level kernels (smem)
+template <int LPL> constexpr int nwg() { return 2; }   // warps per CTA, level kernels: small CTAs spread the few tasks of the top levels over all SMs
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
-constexpr int kRootCH = 8, kRootNS = 4;
-constexpr int kLevCH = 4, kLevNS = 4;
+constexpr int kRootCH = 16, kRootNS = 2;
+constexpr int kLevCH = 8, kLevNS = 2;
+static_assert(kRootCH <= 16 && kLevCH <= 16, "pair_range_ok (capi.cu) allows 16 unnormalised steps");
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
@@ -188,7 +189,10 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         this->dec(ra, ra + kOffB, v, ba, bb);
         if (++cidx == ccount) chunk_release();
     }
-    // passes, as Task::run_pass in hm.cu
+    // passes, as Task::run_pass in hm.cu.  Inside a chunk phi is left
+    // unnormalised (min drifts up by <= span per step; pair_range_ok bounds
+    // kChunkMax steps of drift); it is normalised at the chunk end and before
+    // a spine store.
     template <int DIR>
     __device__ __forceinline__ void run_pass(int first, int nsteps, MP<LPL>& phi) {
         if (nsteps < 1) return;
@@ -196,13 +200,23 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         const int len0 = nsteps + 1;
         int kk = DIR > 0 ? (31 - __clz(len0)) - 1 : 31 - __clz(len0 - 1);
         int target = DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1);
-        auto step = [&](const unsigned (&v)[LPL], int ba, int bb, int s) {
+        unsigned G = 0u;      // min of the current phi.m (packed)
+        int gA = 0, gB = 0;
+        auto normalise = [&]() {
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) phi.m[e] += v[e];
+            for (int e = 0; e < LPL; ++e) phi.m[e] = __vsub2(phi.m[e], G);
+            phi.a += gA; phi.b += gB;
+            G = 0u; gA = 0; gB = 0;
+        };
+        auto step = [&](const unsigned (&v)[LPL], int ba, int bb) {
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) phi.m[e] += v[e];     // both >= 0 per half: no carry
             phi.a += ba; phi.b += bb;
+            G = dtrans2<LPL, PAD, WIN, false>(phi.m, this->ws, this->wsT, this->lane, this->K, gA, gB);
         };
         auto spine = [&](int s) {
             if (s + 2 == target) {
+                normalise();
                 this->st_spine(DIR > 0, first + DIR * (s + 1), phi);
                 --kk;
                 target = kk < 0 ? INT_MAX : (DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1));
@@ -213,7 +227,7 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         while (s < nsteps) {
             chunk_wait();
             const unsigned base = ring + cslot * slotB;
-            if (ccount == kCH) {
+            if (ccount == kCH && target - 2 >= s + kCH) {   // full chunk, no spine node: branch free
                 unsigned v[LPL]; int ba, bb;
                 {
                     const unsigned ra = base + (REV ? kCH - 1 : 0) * kStride;
@@ -221,34 +235,32 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
                 }
 #pragma unroll
                 for (int k = 0; k < kCH; ++k) {
-                    step(v, ba, bb, s + k);
+                    unsigned vn[LPL]; int ban = 0, bbn = 0;
                     if (k + 1 < kCH) {
                         const unsigned ra = base + (REV ? kCH - 2 - k : k + 1) * kStride;
-                        this->dec(ra, ra + kOffB, v, ba, bb);
+                        this->dec(ra, ra + kOffB, vn, ban, bbn);
                     }
-                    this->msg_(phi.m, phi.a, phi.b);
-                    spine(s + k);
+                    step(v, ba, bb);
+                    if (k + 1 < kCH) {
+#pragma unroll
+                        for (int e = 0; e < LPL; ++e) v[e] = vn[e];
+                        ba = ban; bb = bbn;
+                    }
                 }
                 s += kCH;
             } else {
                 const int cnt = ccount;
-                unsigned v[LPL]; int ba, bb;
-                {
-                    const unsigned ra = base + (REV ? cnt - 1 : 0) * kStride;
-                    this->dec(ra, ra + kOffB, v, ba, bb);
-                }
 #pragma unroll 1
                 for (int k = 0; k < cnt; ++k) {
-                    step(v, ba, bb, s + k);
-                    if (k + 1 < cnt) {
-                        const unsigned ra = base + (REV ? cnt - 2 - k : k + 1) * kStride;
-                        this->dec(ra, ra + kOffB, v, ba, bb);
-                    }
-                    this->msg_(phi.m, phi.a, phi.b);
+                    unsigned v[LPL]; int ba, bb;
+                    const unsigned ra = base + (REV ? cnt - 1 - k : k) * kStride;
+                    this->dec(ra, ra + kOffB, v, ba, bb);
+                    step(v, ba, bb);
                     spine(s + k);
                 }
                 s += cnt;
             }
+            normalise();
             chunk_release();
         }
     }
