@@ -504,26 +504,33 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
             } else {
                 const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
                 MP<LPL> pl = L, pr = R;
-                const int nf = i - lo, nb = hi - j;
+                // the two passes interleaved (independent chains -> ILP), left
+                // unnormalised until the Handshake (<= 5 steps of drift)
+                const int nf = i - lo, nb = hi - j;     // nb == nf or nf + 1
+                unsigned Gl = 0u, Gr = 0u;
+                int gla = 0, glb = 0, gra = 0, grb = 0;
+                auto stepL = [&](int k) {
+                    unsigned F[LPL]; int ba, bb;
+                    h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) pl.m[e] += F[e];
+                    pl.a += ba; pl.b += bb;
+                    Gl = dtrans2<LPL, PAD, WIN, false>(pl.m, h.ws, h.wsT, lane, h.K, gla, glb);
+                };
+                auto stepR = [&](int k) {
+                    unsigned F[LPL]; int ba, bb;
+                    h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) pr.m[e] += F[e];
+                    pr.a += ba; pr.b += bb;
+                    Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.ws, h.wsT, lane, h.K, gra, grb);
+                };
 #pragma unroll 1
-                for (int s = 0; s < nf || s < nb; ++s) {
-                    if (s < nf) {
-                        unsigned F[LPL]; int ba, bb;
-                        h.dec(fA(lo + s), fA(lo + s) + kOffF, F, ba, bb);
+                for (int s = 0; s < nf; ++s) { stepL(lo + s); stepR(hi - s); }
+                if (nb > nf) stepR(hi - nf);
 #pragma unroll
-                        for (int e = 0; e < LPL; ++e) pl.m[e] += F[e];
-                        pl.a += ba; pl.b += bb;
-                        h.msg_(pl.m, pl.a, pl.b);
-                    }
-                    if (s < nb) {
-                        unsigned F[LPL]; int ba, bb;
-                        h.dec(fA(hi - s), fA(hi - s) + kOffF, F, ba, bb);
-#pragma unroll
-                        for (int e = 0; e < LPL; ++e) pr.m[e] += F[e];
-                        pr.a += ba; pr.b += bb;
-                        h.msg_(pr.m, pr.a, pr.b);
-                    }
-                }
+                for (int e = 0; e < LPL; ++e) { pl.m[e] = __vsub2(pl.m[e], Gl); pr.m[e] = __vsub2(pr.m[e], Gr); }
+                pl.a += gla; pl.b += glb; pr.a += gra; pr.b += grb;
                 unsigned Fi[LPL], Fj[LPL];
                 int bia, bib, bja, bjb;
                 h.dec(fA(i), fA(i) + kOffF, Fi, bia, bib);

@@ -256,8 +256,11 @@ __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, i
     unsigned pji[LPL];
 #pragma unroll
     for (int e = 0; e < LPL; ++e) pji[e] = pr.m[e] + vj[e];
-    int ja = pr.a + bja, jb = pr.b + bjb;
-    msg2<LPL, PAD, WIN>(pji, ja, jb, ws, wsT, lane, K);
+    const int ja = pr.a + bja, jb = pr.b + bjb;       // phi_ji left unnormalised
+    {
+        int g0, g1;
+        dtrans2<LPL, PAD, WIN, false>(pji, ws, wsT, lane, K, g0, g1);
+    }
     // t = floor((m_i - 2 phi_ji) / 2), m_i = phi_L + f_i + phi_ji; true offset C = pl.o + bi - pji.o
     const int ca = pl.a + bia - ja, cb = pl.b + bib - jb;
     const unsigned c0 = pk(ca & 1, cb & 1);
