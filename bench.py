@@ -42,14 +42,14 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def traffic_per_launch():
-    """dram__bytes_read.sum + dram__bytes_write.sum per hm_kernel launch from the
-    committed ncu --set full capture summary (profiles/), or None."""
+def traffic_per_half_step():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one chain-DP half-step
+    (its root + level + leaf launches) from the committed ncu capture summary
+    (profiles/ncu_traffic.json, written by the launch-list capture), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    # written from the latest committed ncu --set full capture (see profiles/README.md)
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("hm_kernel_bytes_per_launch")
+            return json.load(f).get("hm_bytes_per_half_step")
     return None
 
 
@@ -247,7 +247,8 @@ def main():
     cells = W * H * K
     value = world * cells * iters / (ms / 1e3)
 
-    # roofline of the dominant kernel family: hm_kernel (H and V half-steps)
+    # roofline of the dominant kernel: the chain-DP half-step (root + level +
+    # leaf launches of hm2.cu / hm.cu), H and V; one "launch" = one half-step
     hbm, peak_kind = peaks()
     ms_h, n_h = prof["hm_h"]
     ms_v, n_v = prof["hm_v"]
@@ -262,12 +263,13 @@ def main():
     dbytes = KP * W * H
     alg_bytes_per_step = (dbytes + rec) + (iters - 1) * (2 * rec + dbytes) + iters * (2 * rec + dbytes)
     achieved = alg_bytes_per_step * args.steps / ((ms_h + ms_v) / 1e3) / 1e9
-    tr = traffic_per_launch()
+    tr = traffic_per_half_step()
     step_ms_prof = sum(v[0] for v in prof.values()) / args.steps
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": tr, "kernel": "hm_kernel (H+V half-steps)", "peak_kind": peak_kind,
-                "launches": n_h + n_v,
-                "alg_bytes_per_launch": alg_bytes_per_step / (2 * iters),
+                "traffic": tr, "kernel": "chain-DP half-step (root+level+leaf kernels), H and V",
+                "peak_kind": peak_kind, "launches": n_h + n_v, "half_steps": 2 * iters * args.steps,
+                "kernel_family": ctx.kernel_family(),
+                "alg_bytes_per_half_step": alg_bytes_per_step / (2 * iters),
                 "share_of_step": (ms_h + ms_v) / args.steps / step_ms_prof if step_ms_prof else None,
                 "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()}}
 
