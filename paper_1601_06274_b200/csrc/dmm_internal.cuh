@@ -11,7 +11,8 @@
 //   fwdo, bwdo i32 [H][W][2]    pair path: per-chain offsets of the packed scratch messages
 //   labels u8  [H][W]
 // rec = compact lossless K-vector record of REC = 2*KP + 16 bytes:
-//   u16 v[KP] | int32 base | 12 B pad,  value(k) = base + v[k], base = min_k.
+//   u16 v[KP] | int32 base | 12 B pad,  value(k) = base + v[k], base <= min_k
+//   (the int32 kernels store base = min_k, the pair kernels the running offset).
 // Lossless because every stored vector has a span (max - min over labels)
 // below 2^16 (checked at dmm_create).
 // Both chain orientations read a node's K-vector as one contiguous record,

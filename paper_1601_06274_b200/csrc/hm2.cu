@@ -19,7 +19,8 @@ namespace dmm {
 namespace p2 {
 
 constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
-constexpr int kDepth = 4;    // pending right pieces in a leaf block
+constexpr int kDepth = 2;    // pending right pieces in a leaf block (pieces >= 4 nodes push; 12 -> 6 -> 3)
+static_assert(kCMax <= 15, "leaf stack depth 2");
 template <int LPL> constexpr int nwg() { return 2; }   // warps per CTA, level kernels: small CTAs spread the few tasks of the top levels over all SMs
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
 constexpr int kRootCH = 16, kRootNS = 2;
@@ -385,7 +386,12 @@ __device__ __forceinline__ void leaf_emit(const Pass<LPL, VERT, PAD, WIN, FIRST>
     constexpr int REC = Pass<LPL, VERT, PAD, WIN, FIRST>::REC;
     const int lane = h.lane;
     unsigned Dv[LPL], o[LPL], lam[LPL];
-    ld_u8_pair_s<LPL>(dA, dB, lane, h.fbits, Dv);
+    if constexpr (FIRST) {      // the unaries are D*2^F themselves
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) Dv[e] = F[e];
+    } else {
+        ld_u8_pair_s<LPL>(dA, dB, lane, h.fbits, Dv);
+    }
     unsigned l = kBigP;
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
@@ -490,80 +496,45 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         phase ^= 1u;
         auto fA = [&](int k) { return sF + k * kStrideF; };
         auto dA = [&](int k) { return sD + k * kStrideD; };
+        auto emit = [&](int k, const MP<LPL>& Lb, const MP<LPL>& Rb, const unsigned (&F)[LPL], int ba, int bb) {
+            leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(k), dA(k) + kOffD, lo0 + k, Lb, Rb, F, ba, bb, last, bsum);
+        };
+        // pieces of <= 3 nodes: straight-line code (R5 with the splits unrolled)
+        auto small = [&](int lo, int hi, const MP<LPL>& L, const MP<LPL>& R) {
+            unsigned F0[LPL]; int b0a, b0b;
+            h.dec(fA(lo), fA(lo) + kOffF, F0, b0a, b0b);
+            if (lo == hi) {
+                emit(lo, L, R, F0, b0a, b0b);
+                return;
+            }
+            unsigned F1[LPL]; int b1a, b1b;
+            h.dec(fA(lo + 1), fA(lo + 1) + kOffF, F1, b1a, b1b);
+            MP<LPL> pl = L, pr = R;
+            unsigned F2[LPL]; int b2a = 0, b2b = 0;
+            if (hi == lo + 2) {                 // [lo, lo+2]: i = lo, j = lo+1; one backward step
+                h.dec(fA(lo + 2), fA(lo + 2) + kOffF, F2, b2a, b2b);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) pr.m[e] += F2[e];
+                pr.a += b2a; pr.b += b2b;
+                h.msg_(pr.m, pr.a, pr.b);
+            }
+            handshake2<LPL, PAD, WIN>(F0, b0a, b0b, F1, b1a, b1b, pl, pr, h.ws, h.wsT, lane, h.K);
+            emit(lo, L, pr, F0, b0a, b0b);      // A = [lo, lo] (L, phi_ji')
+            if (hi == lo + 1) {
+                emit(lo + 1, pl, R, F1, b1a, b1b);
+            } else {                            // B = [lo+1, lo+2] (phi_ij, R): i = lo+1, j = lo+2
+                MP<LPL> ql = pl, qr = R;
+                handshake2<LPL, PAD, WIN>(F1, b1a, b1b, F2, b2a, b2b, ql, qr, h.ws, h.wsT, lane, h.K);
+                emit(lo + 1, pl, qr, F1, b1a, b1b);
+                emit(lo + 2, ql, R, F2, b2a, b2b);
+            }
+        };
         int lo = 0, hi = m - 1, sp = 0;
         unsigned stkJ = 0, stkH = 0;
 #pragma unroll 1
         while (true) {
-            bool done_piece = false;
-            if (lo == hi) {
-                unsigned F[LPL]; int ba, bb;
-                h.dec(fA(lo), fA(lo) + kOffF, F, ba, bb);
-                leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(lo), dA(lo) + kOffD, lo0 + lo, L, R, F, ba, bb, last,
-                                                      bsum);
-                done_piece = true;
-            } else {
-                const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
-                MP<LPL> pl = L, pr = R;
-                // the two passes interleaved (independent chains -> ILP), left
-                // unnormalised until the Handshake (<= 5 steps of drift)
-                const int nf = i - lo, nb = hi - j;     // nb == nf or nf + 1
-                unsigned Gl = 0u, Gr = 0u;
-                int gla = 0, glb = 0, gra = 0, grb = 0;
-                auto stepL = [&](int k) {
-                    unsigned F[LPL]; int ba, bb;
-                    h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
-#pragma unroll
-                    for (int e = 0; e < LPL; ++e) pl.m[e] += F[e];
-                    pl.a += ba; pl.b += bb;
-                    Gl = dtrans2<LPL, PAD, WIN, false>(pl.m, h.ws, h.wsT, lane, h.K, gla, glb);
-                };
-                auto stepR = [&](int k) {
-                    unsigned F[LPL]; int ba, bb;
-                    h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
-#pragma unroll
-                    for (int e = 0; e < LPL; ++e) pr.m[e] += F[e];
-                    pr.a += ba; pr.b += bb;
-                    Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.ws, h.wsT, lane, h.K, gra, grb);
-                };
-#pragma unroll 1
-                for (int s = 0; s < nf; ++s) { stepL(lo + s); stepR(hi - s); }
-                if (nb > nf) stepR(hi - nf);
-#pragma unroll
-                for (int e = 0; e < LPL; ++e) { pl.m[e] = __vsub2(pl.m[e], Gl); pr.m[e] = __vsub2(pr.m[e], Gr); }
-                pl.a += gla; pl.b += glb; pr.a += gra; pr.b += grb;
-                unsigned Fi[LPL], Fj[LPL];
-                int bia, bib, bja, bjb;
-                h.dec(fA(i), fA(i) + kOffF, Fi, bia, bib);
-                h.dec(fA(j), fA(j) + kOffF, Fj, bja, bjb);
-                handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.ws, h.wsT, lane, h.K);
-                // children: A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R)
-                const bool leafA = (i == lo), leafB = (j == hi);
-                if (leafA)
-                    leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(i), dA(i) + kOffD, lo0 + i, L, pr, Fi, bia, bib, last,
-                                                          bsum);
-                if (leafB)
-                    leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(j), dA(j) + kOffD, lo0 + j, pl, R, Fj, bja, bjb, last,
-                                                          bsum);
-                if (leafA && leafB) {
-                    done_piece = true;
-                } else if (leafA) {
-                    lo = j;
-                    L = pl;
-                } else if (leafB) {
-                    hi = i;
-                    R = pr;
-                } else {                            // push B, continue with A
-                    stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
-                    stkH = (stkH & ~(0xfu << (4 * sp))) | ((unsigned)hi << (4 * sp));
-                    __syncwarp();
-                    st_mp_s<LPL>(stk + (2 * sp) * SMP, lane, pl);
-                    st_mp_s<LPL>(stk + (2 * sp + 1) * SMP, lane, R);
-                    ++sp;
-                    hi = i;
-                    R = pr;
-                }
-            }
-            if (done_piece) {
+            if (hi - lo < 3) {
+                small(lo, hi, L, R);
                 if (sp == 0) break;
                 --sp;
                 lo = (int)((stkJ >> (4 * sp)) & 0xfu);
@@ -571,7 +542,52 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
                 __syncwarp();
                 ld_mp_s<LPL>(stk + (2 * sp) * SMP, lane, L);
                 ld_mp_s<LPL>(stk + (2 * sp + 1) * SMP, lane, R);
+                continue;
             }
+            const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
+            MP<LPL> pl = L, pr = R;
+            // the two passes interleaved (independent chains -> ILP), left
+            // unnormalised until the Handshake (<= 5 steps of drift)
+            const int nf = i - lo, nb = hi - j;     // nb == nf or nf + 1
+            unsigned Gl = 0u, Gr = 0u;
+            int gla = 0, glb = 0, gra = 0, grb = 0;
+            auto stepL = [&](int k) {
+                unsigned F[LPL]; int ba, bb;
+                h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) pl.m[e] += F[e];
+                pl.a += ba; pl.b += bb;
+                Gl = dtrans2<LPL, PAD, WIN, false>(pl.m, h.ws, h.wsT, lane, h.K, gla, glb);
+            };
+            auto stepR = [&](int k) {
+                unsigned F[LPL]; int ba, bb;
+                h.dec(fA(k), fA(k) + kOffF, F, ba, bb);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) pr.m[e] += F[e];
+                pr.a += ba; pr.b += bb;
+                Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.ws, h.wsT, lane, h.K, gra, grb);
+            };
+#pragma unroll 1
+            for (int s = 0; s < nf; ++s) { stepL(lo + s); stepR(hi - s); }
+            if (nb > nf) stepR(hi - nf);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) { pl.m[e] = __vsub2(pl.m[e], Gl); pr.m[e] = __vsub2(pr.m[e], Gr); }
+            pl.a += gla; pl.b += glb; pr.a += gra; pr.b += grb;
+            unsigned Fi[LPL], Fj[LPL];
+            int bia, bib, bja, bjb;
+            h.dec(fA(i), fA(i) + kOffF, Fi, bia, bib);
+            h.dec(fA(j), fA(j) + kOffF, Fj, bja, bjb);
+            handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.ws, h.wsT, lane, h.K);
+            // children A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R), both >= 2
+            // nodes: push B, continue with A
+            stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
+            stkH = (stkH & ~(0xfu << (4 * sp))) | ((unsigned)hi << (4 * sp));
+            __syncwarp();
+            st_mp_s<LPL>(stk + (2 * sp) * SMP, lane, pl);
+            st_mp_s<LPL>(stk + (2 * sp + 1) * SMP, lane, R);
+            ++sp;
+            hi = i;
+            R = pr;
         }
         __syncwarp();
     }

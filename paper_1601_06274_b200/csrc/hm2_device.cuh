@@ -196,21 +196,16 @@ __device__ __forceinline__ void ld_u8_pair_s(unsigned da, unsigned db, int lane,
     }
 }
 
-// Store the pair o (packed, >= 0 per half, offsets oa / ob) as two compact
-// records (base = min over labels < K); B only if wb.
+// Store the pair o (packed, 0 <= o <= span bound per half, offsets oa / ob)
+// as two compact records with base = the offset and v = o: a valid record
+// (base <= min, span < 2^16) without a warp reduction.  B only if wb.
 template <int LPL, bool PAD>
-__device__ __forceinline__ void st_rec_pair(uint8_t* ra, uint8_t* rb, bool wb, int lane, unsigned (&o)[LPL], int oa,
-                                            int ob, int K) {
+__device__ __forceinline__ void st_rec_pair(uint8_t* ra, uint8_t* rb, bool wb, int lane, const unsigned (&o)[LPL],
+                                            int oa, int ob, int K) {
     constexpr int KP = 32 * LPL;
-    unsigned l = kBigP;
-#pragma unroll
-    for (int e = 0; e < LPL; ++e)
-        if (!PAD || lane * LPL + e < K) l = __vmins2(l, o[e]);
-    const int gA = __reduce_min_sync(kFull, lo16(l)), gB = __reduce_min_sync(kFull, hi16(l));
-    const unsigned G = pk(gA, gB);
     unsigned v[LPL];
 #pragma unroll
-    for (int e = 0; e < LPL; ++e) v[e] = (!PAD || lane * LPL + e < K) ? o[e] - G : 0u;
+    for (int e = 0; e < LPL; ++e) v[e] = (!PAD || lane * LPL + e < K) ? o[e] : 0u;
     uint8_t* pa = ra + 2 * LPL * lane;
     uint8_t* pb = rb + 2 * LPL * lane;
     if constexpr (LPL == 1) {
@@ -234,8 +229,8 @@ __device__ __forceinline__ void st_rec_pair(uint8_t* ra, uint8_t* rb, bool wb, i
                            __byte_perm(v[4], v[5], 0x7632), __byte_perm(v[6], v[7], 0x7632));
     }
     if (lane == 0) {
-        *reinterpret_cast<int32_t*>(ra + 2 * KP) = oa + gA;
-        if (wb) *reinterpret_cast<int32_t*>(rb + 2 * KP) = ob + gB;
+        *reinterpret_cast<int32_t*>(ra + 2 * KP) = oa;
+        if (wb) *reinterpret_cast<int32_t*>(rb + 2 * KP) = ob;
     }
 }
 
