@@ -73,7 +73,10 @@ bool pair_range_ok(const dmm_config* c) {
     const long long w = c->w_h > c->w_v ? c->w_h : c->w_v;
     const long long T = c->trunc < K ? c->trunc : K;
     const long long wsT = (w << c->frac_bits) * T;
-    return 16 * span_bound(c) + 3 * wsT + 4 <= 16383;
+    const int bits = (2 * c->census_radius + 1) * (2 * c->census_radius + 1) - 1;
+    const int oob = c->oob_cost >= 0 ? c->oob_cost : bits / 2;
+    // D < 128: the packed D unpack zero-fills with sign-replicated bytes
+    return 16 * span_bound(c) + 3 * wsT + 4 <= 16383 && oob < 128 && bits < 128;
 }
 
 int kp_of(int K) {

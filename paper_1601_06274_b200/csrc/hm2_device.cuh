@@ -25,6 +25,12 @@ constexpr unsigned kBigP = 0x3fff3fffu;
 constexpr unsigned kNegBigP = 0xc001c001u;
 
 __device__ __forceinline__ unsigned pk(int lo, int hi) { return __byte_perm((unsigned)lo, (unsigned)hi, 0x5410); }
+// PTX prmt with the sign-replicate selector bit (__byte_perm masks it off)
+__device__ __forceinline__ unsigned prmt_sgn(unsigned a, unsigned b, unsigned sel) {
+    unsigned r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
 __device__ __forceinline__ int lo16(unsigned x) { return (int)(short)(x & 0xffffu); }
 __device__ __forceinline__ int hi16(unsigned x) { return ((int)x) >> 16; }
 
@@ -91,13 +97,15 @@ __device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], int ws_, int wsT
         inf = __shfl_up_sync(kFull, cf, 1);
         inb = __shfl_down_sync(kFull, cb, 1);
     }
-    if (lane == 0) inf = big;
-    if (lane == 31) inb = big;
+    // Lanes 0 / 31 have no left / right neighbour: the shuffle returned one of
+    // their own (real, >= min) values, so the addend wsT + 1 puts that candidate
+    // above the cap (no select needed).
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
         const bool needL = WIN > 0 ? (e + 1 < WIN) : true;
         const bool needR = WIN > 0 ? (LPL - e < WIN) : true;
-        const int al = min(ws_ * (e + 1), clampv), ar = min(ws_ * (LPL - e), clampv);
+        const int al = lane == 0 ? clampv : min(ws_ * (e + 1), clampv);
+        const int ar = lane == 31 ? clampv : min(ws_ * (LPL - e), clampv);
         const unsigned vf = needL ? addop2<MAX>(inf, pk(sg * al, sg * al), fw[e]) : fw[e];
         const unsigned vb = needR ? addop2<MAX>(inb, pk(sg * ar, sg * ar), bw[e]) : bw[e];
         x[e] = op3_2<MAX>(vf, vb, cap);
@@ -179,19 +187,23 @@ __device__ __forceinline__ void ld_u8_pair_s(unsigned da, unsigned db, int lane,
         v[0] = __byte_perm(a, b, 0x3420) << fbits;
         v[1] = __byte_perm(a, b, 0x3521) << fbits;
     } else if constexpr (LPL == 4) {
+        // bytes [a_e, sign(a_e), b_e, sign(b_e)]: D < 128 (pair_range_ok) makes
+        // the sign-replicated bytes zero; the scale runs on the FMA pipe
         const unsigned a = lds32(da + o), b = lds32(db + o);
+        const unsigned sc = 1u << fbits;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const unsigned sel = (unsigned)(e | (e << 4) | ((4 + e) << 8) | ((4 + e) << 12));
-            v[e] = (__byte_perm(a, b, sel) & 0x00ff00ffu) << fbits;
+            const unsigned sel = (unsigned)(e | ((e | 8) << 4) | ((4 + e) << 8) | (((4 + e) | 8) << 12));
+            v[e] = prmt_sgn(a, b, sel) * sc;
         }
     } else {
         const uint2 a = lds64(da + o), b = lds64(db + o);
+        const unsigned sc = 1u << fbits;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const unsigned sel = (unsigned)(e | (e << 4) | ((4 + e) << 8) | ((4 + e) << 12));
-            v[e] = (__byte_perm(a.x, b.x, sel) & 0x00ff00ffu) << fbits;
-            v[4 + e] = (__byte_perm(a.y, b.y, sel) & 0x00ff00ffu) << fbits;
+            const unsigned sel = (unsigned)(e | ((e | 8) << 4) | ((4 + e) << 8) | (((4 + e) | 8) << 12));
+            v[e] = prmt_sgn(a.x, b.x, sel) * sc;
+            v[4 + e] = prmt_sgn(a.y, b.y, sel) * sc;
         }
     }
 }

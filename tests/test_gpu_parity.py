@@ -111,6 +111,8 @@ def test_kernel_family_selection():
     assert c3.kernel_family() == "pair"
     big = _ctx(width=64, height=8, d_min=0, d_max=99, w_h=5, w_v=2, T=7, frac_bits=8)
     assert big.kernel_family() == "int32"
+    oob = _ctx(width=64, height=8, d_min=0, d_max=15, w=1, T=1, frac_bits=0, oob_cost=200)
+    assert oob.kernel_family() == "int32"      # D >= 128: packed D unpack needs D < 128
     c2.set_pair(False)
     assert c2.kernel_family() == "int32"
 
