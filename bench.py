@@ -166,7 +166,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3"))
+    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C5"),
+                    help="C2 (default): one KITTI frame per GPU per step; C5: configs[4], 64 KITTI frames per "
+                         "step sharded over the GPUs, each GPU solving its frames as one batch (throughput mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--mode", choices=("frames", "bands"), default="frames",
@@ -196,18 +198,26 @@ def main():
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
     if args.mode == "bands":
         return run_bands(args, c, world, rank, local, dev)
-    left, right, _ = datagen.pair(c["kind"], W, H, K, seed=rank)   # one frame per rank
+    total_frames = c.get("frames", world)          # C2: one frame per rank; C5: 64 frames per step
+    nf = (total_frames + world - 1) // world
+    distinct = [datagen.pair(c["kind"], W, H, K, seed=rank * nf + s) for s in range(min(nf, 8))]
+    left, right = distinct[0][0], distinct[0][1]
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
-                      max_iters=iters, device=dev)
+                      max_iters=iters, batch=nf, device=dev)
     if args.wave_mb is not None:
         ctx.set_wave_bytes(int(args.wave_mb * (1 << 20)))
-    lt = torch.from_numpy(left).to(dev)
-    rt = torch.from_numpy(right).to(dev)
+    Lh = np.stack([distinct[s % len(distinct)][0] for s in range(nf)])
+    Rh = np.stack([distinct[s % len(distinct)][1] for s in range(nf)])
+    lt = torch.from_numpy(Lh).to(dev)
+    rt = torch.from_numpy(Rh).to(dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        ctx.cost_volume(lt, rt, stream=stream)
-        ctx.solve(iters, stream=stream)
+        if nf == 1:
+            ctx.cost_volume(lt[0], rt[0], stream=stream)
+        else:
+            ctx.cost_volume_frames(lt, rt, stream=stream)
+        ctx.solve(iters, frame=0, nframes=nf, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -245,7 +255,7 @@ def main():
         ms = float(t.item())
 
     cells = W * H * K
-    value = world * cells * iters / (ms / 1e3)
+    value = world * nf * cells * iters / (ms / 1e3)
 
     # roofline of the dominant kernel: the chain-DP half-step (root + level +
     # leaf launches of hm2.cu / hm.cu), H and V; one "launch" = one half-step
@@ -261,7 +271,7 @@ def main():
         KP *= 2
     rec = (2 * KP + 16) * W * H
     dbytes = KP * W * H
-    alg_bytes_per_step = (dbytes + rec) + (iters - 1) * (2 * rec + dbytes) + iters * (2 * rec + dbytes)
+    alg_bytes_per_step = nf * ((dbytes + rec) + (iters - 1) * (2 * rec + dbytes) + iters * (2 * rec + dbytes))
     achieved = alg_bytes_per_step * args.steps / ((ms_h + ms_v) / 1e3) / 1e9
     tr = traffic_per_half_step()
     step_ms_prof = sum(v[0] for v in prof.values()) / args.steps
@@ -276,11 +286,18 @@ def main():
     # end to end through the public C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        lh = torch.from_numpy(left).pin_memory()
-        rh = torch.from_numpy(right).pin_memory()
-        lab = torch.empty((H, W), dtype=torch.uint8).pin_memory()
+        lh = torch.from_numpy(Lh).pin_memory()
+        rh = torch.from_numpy(Rh).pin_memory()
+        lab = torch.empty((nf, H, W), dtype=torch.uint8).pin_memory()
+
+        def host_step():
+            if nf == 1:
+                ctx.run_host(lh[0], rh[0], iters, labels_out=lab[0], stream=stream)
+            else:
+                ctx.run_host_frames(lh, rh, iters, labels_out=lab, stream=stream)
+
         for _ in range(2):
-            ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
+            host_step()
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -289,7 +306,7 @@ def main():
         t0.record(stream)
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
+            host_step()
         t1.record(stream)
         torch.cuda.synchronize(dev)
         wall_ms = (time.perf_counter() - w0) * 1e3 / args.steps
@@ -298,8 +315,9 @@ def main():
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": world * cells * iters / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * W * H, "d2h_bytes_per_step": W * H + 8 + 16 * iters,
+        e2e = {"value": world * nf * cells * iters / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": nf * 2 * W * H,
+               "d2h_bytes_per_step": nf * (W * H + 16) if nf > 1 else W * H + 8 + 16 * iters,
                "ms_per_step": ems}
 
     cpu = None
@@ -314,9 +332,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"{args.config}: stereo {W}x{H}, {K} disparities, census 5x5, "
-                                   f"{iters} dual iterations, warped-texture pair, 1 frame per GPU",
+                                   f"{iters} dual iterations, warped-texture pairs, "
+                                   + ("1 frame per GPU" if nf == 1 else
+                                      f"{total_frames} frames per step ({nf} per GPU, solved as one batch)"),
                        "W": W, "H": H, "K": K, "iters": iters, "w": W_REG, "T": T_REG, "frac_bits": FBITS,
-                       "fps": world / (ms / 1e3), "parallelism": f"frames x{world}",
+                       "frames_per_gpu": nf,
+                       "fps": world * nf / (ms / 1e3), "parallelism": f"frames x{world}",
                        "l2": "flushed between timed steps (256 MB write outside events); step working set ~1 GB"},
             "roofline": roofline,
             "cpu_baseline": cpu,

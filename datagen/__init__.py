@@ -122,6 +122,8 @@ CONFIGS = {
     "C1": dict(W=64, H=48, K=16, d_min=0, iters=5, kind="rd"),
     "C2": dict(W=1242, H=375, K=128, d_min=0, iters=4, kind="wt-kitti"),
     "C3": dict(W=1500, H=1000, K=256, d_min=0, iters=4, kind="wt-middlebury"),
+    # configs[4]: a stream of 64 KITTI-shaped pairs, frames sharded over the GPUs
+    "C5": dict(W=1242, H=375, K=128, d_min=0, iters=4, kind="wt-kitti", frames=64),
 }
 
 

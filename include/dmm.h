@@ -122,6 +122,20 @@ DMM_API dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_hos
                         const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
                         int64_t* energy, int64_t* bound, void* stream);
 
+/* Batched forms for a stream of frames (BASELINE configs[4], throughput mode):
+ * frames [frame, frame + nframes) in one launch per kernel.
+ * dmm_cost_volume_frames: left/right device images stacked [nframes][height]
+ *   rows of `pitch` bytes (pitch >= width); DMM_E_ARG / DMM_E_SHAPE as
+ *   dmm_cost_volume, and frame ranges outside [0, batch).
+ * dmm_run_host_frames: dmm_run_host for nframes frames: host images and
+ *   labels stacked u8 [nframes][H][W]; energy[f], bound[f] (nframes entries
+ *   each, scaled by 2^F).  Synchronises `stream`. */
+DMM_API dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left,
+                                          const uint8_t* right, int64_t pitch, void* stream);
+DMM_API dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left_host,
+                                       const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
+                                       int64_t* energy, int64_t* bound, void* stream);
+
 /* ---- chain-DP primitives (no context; device int32 arrays, dense
  * [count][K], K in [1, 256], ws = w * 2^F >= 0, T >= 1).  They run exactly the
  * device code of the Dual MM kernels, one warp per K-vector.

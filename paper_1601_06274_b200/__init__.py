@@ -27,6 +27,7 @@ EXPORTS = (
     "dmm_run_host", "dmm_launch_count", "dmm_status_str", "dmm_last_error",
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
+    "dmm_cost_volume_frames", "dmm_run_host_frames",
 )
 BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
 TUNE_WAVE_BYTES = 1
@@ -72,6 +73,8 @@ def load_library():
         "dmm_copy_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P]),
         "dmm_copy_dual": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P]),
         "dmm_run_host": (ctypes.c_int, [P, ctypes.c_int, P, P, i32, P, P, P, P]),
+        "dmm_cost_volume_frames": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, i64, P]),
+        "dmm_run_host_frames": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, i32, P, P, P, P]),
         "dmm_launch_count": (i64, [P]),
         "dmm_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "dmm_last_error": (ctypes.c_char_p, [P]),
@@ -231,6 +234,18 @@ class Context:
         self._call("dmm_cost_volume", frame, ctypes.c_void_p(left.data_ptr()),
                    ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream))
 
+    def cost_volume_frames(self, left, right, frame: int = 0, stream=None):
+        """left/right: torch.uint8 (nframes, H, W) contiguous stacks on this device:
+        census + cost volume of frames [frame, frame + nframes) in one launch each."""
+        for t in (left, right):
+            if (t.dtype.itemsize != 1 or t.device != self.device or t.dim() != 3 or not t.is_contiguous()
+                    or tuple(t.shape[1:]) != (self.H, self.W)):
+                raise DmmError("images must be contiguous uint8 (nframes, H, W) tensors on the context device")
+        if left.shape[0] != right.shape[0]:
+            raise DmmError("left/right frame counts differ")
+        self._call("dmm_cost_volume_frames", frame, int(left.shape[0]), ctypes.c_void_p(left.data_ptr()),
+                   ctypes.c_void_p(right.data_ptr()), self.W, _stream_handle(stream))
+
     def solve(self, iterations: int = 4, frame: int = 0, nframes: int = 1, stream=None):
         self._call("dmm_solve", frame, nframes, iterations, _stream_handle(stream))
         for f in range(frame, frame + nframes):
@@ -308,6 +323,25 @@ class Context:
         e = ctypes.c_int64()
         self._call("dmm_energy", frame, ctypes.byref(e), _stream_handle(stream))
         return int(e.value)
+
+    def run_host_frames(self, left, right, iterations: int = 4, labels_out=None, frame: int = 0, stream=None):
+        """run_host for a stack of frames: host uint8 (nframes, H, W) buffers
+        (contiguous, preferably pinned).  Returns (labels, energies, bounds)."""
+        import torch
+        n = int(left.shape[0])
+        for t in (left, right):
+            if t.device.type != "cpu" or not t.is_contiguous() or tuple(t.shape) != (n, self.H, self.W):
+                raise DmmError("run_host_frames expects contiguous host (nframes, H, W) uint8 buffers")
+        if labels_out is None:
+            labels_out = torch.empty((n, self.H, self.W), dtype=torch.uint8).pin_memory()
+        e = (ctypes.c_int64 * n)()
+        b = (ctypes.c_int64 * n)()
+        self._call("dmm_run_host_frames", frame, n, ctypes.c_void_p(left.data_ptr()),
+                   ctypes.c_void_p(right.data_ptr()), iterations, ctypes.c_void_p(labels_out.data_ptr()), e, b,
+                   _stream_handle(stream))
+        for f in range(frame, frame + n):
+            self._iters[f] = iterations
+        return labels_out, [int(v) for v in e], [int(v) for v in b]
 
     def run_host(self, left, right, iterations: int = 4, labels_out=None, frame: int = 0, stream=None):
         """End-to-end through the C ABI with HOST buffers (numpy or CPU tensors,

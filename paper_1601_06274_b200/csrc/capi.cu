@@ -386,6 +386,54 @@ dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const
     return dmm_result(ctx, frame, energy, bound, nullptr, stream);
 }
 
+dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left,
+                                  const uint8_t* right, int64_t pitch, void* stream) {
+    dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st) return st;
+    if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
+    if (pitch < ctx->cfg.width) { ctx->err = "pitch < width"; return DMM_E_SHAPE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, nframes, ctx->cfg.census_radius, pitch, left, right, s); }
+    { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, nframes, ctx->cfg.d_min, ctx->oob, s); }
+    if ((st = check_launch(ctx, "cost_volume_frames"))) return st;
+    for (int f = frame; f < frame + nframes; ++f) { ctx->has_cost[f] = 1; ctx->iters_done[f] = 0; }
+    return DMM_OK;
+}
+
+dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left_host,
+                               const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
+                               int64_t* energy, int64_t* bound, void* stream) {
+    dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st) return st;
+    if (!left_host || !right_host || !labels_host || !energy || !bound) return DMM_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    const size_t px = (size_t)ctx->L.W * ctx->L.H, fb = ctx->L.frame_bytes;
+    // host [nframes][px] <-> the frames' staging / label arrays (stride frame_bytes)
+    if ((st = cuda_err(ctx, cudaMemcpy2DAsync(P.img_l, fb, left_host, px, px, nframes, cudaMemcpyHostToDevice, s),
+                       "h2d")))
+        return st;
+    if ((st = cuda_err(ctx, cudaMemcpy2DAsync(P.img_r, fb, right_host, px, px, nframes, cudaMemcpyHostToDevice, s),
+                       "h2d")))
+        return st;
+    { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, nframes, ctx->cfg.census_radius, ctx->L.W, nullptr, nullptr, s); }
+    { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, nframes, ctx->cfg.d_min, ctx->oob, s); }
+    if ((st = check_launch(ctx, "run_host_frames"))) return st;
+    for (int f = frame; f < frame + nframes; ++f) { ctx->has_cost[f] = 1; ctx->iters_done[f] = 0; }
+    if ((st = dmm_solve(ctx, frame, nframes, iterations, stream))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpy2DAsync(labels_host, px, P.labels, fb, px, nframes, cudaMemcpyDeviceToHost, s),
+                       "d2h")))
+        return st;
+    if ((st = cuda_err(ctx, cudaMemcpy2DAsync(energy, 8, P.energy, fb, 8, nframes, cudaMemcpyDeviceToHost, s),
+                       "d2h energy")))
+        return st;
+    if ((st = cuda_err(ctx, cudaMemcpy2DAsync(bound, 8, P.bounds + 2 * iterations - 1, fb, 8, nframes,
+                                              cudaMemcpyDeviceToHost, s),
+                       "d2h bound")))
+        return st;
+    return cuda_err(ctx, cudaStreamSynchronize(s), "sync");
+}
+
 dmm_status dmm_buffer_ptr(dmm_ctx* ctx, int frame, int which, void** ptr, size_t* bytes, int* bytes_per_pixel) {
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;

@@ -172,6 +172,27 @@ def test_errors():
         dmm.Context(width=16, height=8, d_min=0, d_max=300)   # K > 256
 
 
+def test_frame_stack_apis(orc):
+    """dmm_cost_volume_frames + dmm_solve(nframes) and dmm_run_host_frames
+    (configs[4]-style streams) equal the oracle frame by frame."""
+    W, H, K, iters, n = 70, 37, 32, 3, 3
+    pairs = [datagen.pair("wt-kitti", W, H, K, seed=20 + s) for s in range(n)]
+    L = torch.from_numpy(np.stack([p[0] for p in pairs]))
+    R = torch.from_numpy(np.stack([p[1] for p in pairs]))
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, batch=n, max_iters=iters)
+    ctx.cost_volume_frames(L.cuda(), R.cuda())
+    ctx.solve(iters, frame=0, nframes=n)
+    orcs = [_run_oracle(orc, p[0], p[1], 0, K, 3, 3, 4, 4, iters) for p in pairs]
+    for f in range(n):
+        e, b, hist = ctx.result(frame=f)
+        assert np.array_equal(ctx.labels(frame=f).cpu().numpy().astype(np.int32), orcs[f]["labels"])
+        assert np.array_equal(np.array(hist), orcs[f]["bound_hist"]) and e == orcs[f]["energy"]
+    lab, es, bs = ctx.run_host_frames(L.pin_memory(), R.pin_memory(), iters)
+    for f in range(n):
+        assert np.array_equal(lab[f].numpy().astype(np.int32), orcs[f]["labels"])
+        assert es[f] == orcs[f]["energy"] and bs[f] == orcs[f]["bound_hist"][-1]
+
+
 @pytest.mark.slow
 def test_c2_full_size(orc):
     """configs[1] at full size (1242x375x128, 4 iterations), in the launch
