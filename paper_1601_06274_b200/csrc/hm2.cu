@@ -484,10 +484,20 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
                 }
             }
         }
-        MP<LPL> L, R;
+        MP<LPL> L, R, Kp;
+        // Fig.11 reuse for the block's first split: a left block keeps its left
+        // boundary, so the message into its split node from the left is on the
+        // fwd spine (stored by the pass that produced L); a right block finds the
+        // one from the right on the bwd spine.  Only the other pass is computed.
+        int keep = 0;
         if (lstar > 0) {
             h.ld_spine(true, lo0, L);
             h.ld_spine(false, hi0, R);
+            if (m >= 4) {
+                const int ib = m / 2 - 1;
+                if (!(b & 1)) { h.ld_spine(true, lo0 + ib, Kp); keep = 1; }
+                else { h.ld_spine(false, lo0 + ib + 1, Kp); keep = 2; }
+            }
         } else {
             L.zero(); R.zero();
         }
@@ -567,9 +577,21 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
                 pr.a += ba; pr.b += bb;
                 Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.ws, h.wsT, lane, h.K, gra, grb);
             };
+            const int kp = keep;
+            keep = 0;
+            if (kp == 1) {                  // phi into i from the left: fwd spine
+                pl = Kp;
 #pragma unroll 1
-            for (int s = 0; s < nf; ++s) { stepL(lo + s); stepR(hi - s); }
-            if (nb > nf) stepR(hi - nf);
+                for (int s = 0; s < nb; ++s) stepR(hi - s);
+            } else if (kp == 2) {           // phi into j from the right: bwd spine
+                pr = Kp;
+#pragma unroll 1
+                for (int s = 0; s < nf; ++s) stepL(lo + s);
+            } else {
+#pragma unroll 1
+                for (int s = 0; s < nf; ++s) { stepL(lo + s); stepR(hi - s); }
+                if (nb > nf) stepR(hi - nf);
+            }
 #pragma unroll
             for (int e = 0; e < LPL; ++e) { pl.m[e] = __vsub2(pl.m[e], Gl); pr.m[e] = __vsub2(pr.m[e], Gr); }
             pl.a += gla; pl.b += glb; pr.a += gra; pr.b += grb;
