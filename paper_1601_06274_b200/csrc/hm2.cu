@@ -48,6 +48,7 @@ struct Pass {
     int W, K, cA, cB, lane, n, nch;
     bool hasB;
     int fbits, ws, wsT;
+    DtK<LPL> dk;
 
     __device__ __forceinline__ void init(const PassArgs& a, int lane_) {
         P = frame_ptrs(a.L, a.frame0 + blockIdx.y);
@@ -57,6 +58,7 @@ struct Pass {
         n = VERT ? a.L.H : a.L.W;
         nch = VERT ? a.L.W : a.L.H;
         fbits = a.fbits; ws = a.ws; wsT = a.wsT;
+        dk.init(ws, wsT, K, lane);
     }
     __device__ __forceinline__ void set_pair(int pc) {
         cA = 2 * pc;
@@ -67,7 +69,7 @@ struct Pass {
     __device__ __forceinline__ int qA(int p) const { return q_of(cA, p); }
     __device__ __forceinline__ int qB(int p) const { return q_of(cB, p); }
     __device__ __forceinline__ void msg_(unsigned (&x)[LPL], int& oa, int& ob) const {
-        msg2<LPL, PAD, WIN>(x, oa, ob, ws, wsT, lane, K);
+        msg2<LPL, PAD, WIN>(x, oa, ob, dk);
     }
     // staged source pair (records, or D rows when FIRST) -> packed values + bases
     __device__ __forceinline__ void dec(unsigned ra, unsigned rb, unsigned (&v)[LPL], int& ba, int& bb) const {
@@ -213,7 +215,7 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi.m[e] += v[e];     // both >= 0 per half: no carry
             phi.a += ba; phi.b += bb;
-            G = dtrans2<LPL, PAD, WIN, false>(phi.m, this->ws, this->wsT, this->lane, this->K, gA, gB);
+            G = dtrans2<LPL, PAD, WIN, false>(phi.m, this->dk, gA, gB);
         };
         auto spine = [&](int s) {
             if (s + 2 == target) {
@@ -271,7 +273,7 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         int bia, bib, bja, bjb;
         pop(vj, bja, bjb);
         pop(vi, bia, bib);
-        handshake2<LPL, PAD, WIN>(vi, bia, bib, vj, bja, bjb, pl, pr, this->ws, this->wsT, this->lane, this->K);
+        handshake2<LPL, PAD, WIN>(vi, bia, bib, vj, bja, bjb, pl, pr, this->dk);
         this->st_spine(true, i + 1, pl);
         this->st_spine(false, i, pr);
     }
@@ -528,13 +530,13 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
                 pr.a += b2a; pr.b += b2b;
                 h.msg_(pr.m, pr.a, pr.b);
             }
-            handshake2<LPL, PAD, WIN>(F0, b0a, b0b, F1, b1a, b1b, pl, pr, h.ws, h.wsT, lane, h.K);
+            handshake2<LPL, PAD, WIN>(F0, b0a, b0b, F1, b1a, b1b, pl, pr, h.dk);
             emit(lo, L, pr, F0, b0a, b0b);      // A = [lo, lo] (L, phi_ji')
             if (hi == lo + 1) {
                 emit(lo + 1, pl, R, F1, b1a, b1b);
             } else {                            // B = [lo+1, lo+2] (phi_ij, R): i = lo+1, j = lo+2
                 MP<LPL> ql = pl, qr = R;
-                handshake2<LPL, PAD, WIN>(F1, b1a, b1b, F2, b2a, b2b, ql, qr, h.ws, h.wsT, lane, h.K);
+                handshake2<LPL, PAD, WIN>(F1, b1a, b1b, F2, b2a, b2b, ql, qr, h.dk);
                 emit(lo + 1, pl, qr, F1, b1a, b1b);
                 emit(lo + 2, ql, R, F2, b2a, b2b);
             }
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
 #pragma unroll
                 for (int e = 0; e < LPL; ++e) pl.m[e] += F[e];
                 pl.a += ba; pl.b += bb;
-                Gl = dtrans2<LPL, PAD, WIN, false>(pl.m, h.ws, h.wsT, lane, h.K, gla, glb);
+                Gl = dtrans2<LPL, PAD, WIN, false>(pl.m, h.dk, gla, glb);
             };
             auto stepR = [&](int k) {
                 unsigned F[LPL]; int ba, bb;
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
 #pragma unroll
                 for (int e = 0; e < LPL; ++e) pr.m[e] += F[e];
                 pr.a += ba; pr.b += bb;
-                Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.ws, h.wsT, lane, h.K, gra, grb);
+                Gr = dtrans2<LPL, PAD, WIN, false>(pr.m, h.dk, gra, grb);
             };
             const int kp = keep;
             keep = 0;
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
             int bia, bib, bja, bjb;
             h.dec(fA(i), fA(i) + kOffF, Fi, bia, bib);
             h.dec(fA(j), fA(j) + kOffF, Fj, bja, bjb);
-            handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.ws, h.wsT, lane, h.K);
+            handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.dk);
             // children A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R), both >= 2
             // nodes: push B, continue with A
             stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));

@@ -45,33 +45,63 @@ __device__ __forceinline__ unsigned op3_2(unsigned a, unsigned b, unsigned c) {
     return MAX ? __vimax3_s16x2(a, b, c) : __vimin3_s16x2(a, b, c);
 }
 
+// Loop-invariant operands of the packed distance transform, built once per
+// kernel (per lane): ws, wsT, and the min-plus addends of the one-hop window,
+// with wsT + 1 at lanes 0 / 31 (no neighbour: the shuffle returned one of the
+// lane's own values, >= min, so that candidate lands above the cap without a
+// select).  Addends beyond the truncation are clamped to wsT + 1: such a
+// candidate exceeds the cap g + wsT, clamped or not.
+template <int LPL>
+struct DtK {
+    int ws, wsT, K, lane;
+    unsigned wsP, capP;               // pk(ws), pk(wsT)
+    unsigned aL[LPL], aR[LPL];        // per label e: left (e+1)*ws, right (LPL-e)*ws
+    __device__ __forceinline__ void init(int ws_, int wsT_, int K_, int lane_) {
+        ws = ws_; wsT = wsT_; K = K_; lane = lane_;
+        const int cl = wsT + 1;
+        const int w1 = min(ws, cl);
+        wsP = pk(w1, w1);
+        capP = pk(wsT, wsT);
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            const int al = lane == 0 ? cl : min(ws * (e + 1), cl);
+            const int ar = lane == 31 ? cl : min(ws * (LPL - e), cl);
+            aL[e] = pk(al, al);
+            aR[e] = pk(ar, ar);
+        }
+    }
+};
+
 // Packed distance transform of two K-vectors (see dtrans in hm_device.cuh for
 // the windowed / Kogge-Stone structure):
 //   MAX = false: x(b) := min_a x(a) + ws*min(|a-b|, T)      (Msg)
 //   MAX = true:  x(b) := max_a x(a) - ws*min(|a-b|, T)
 // Returns G = pk(gA, gB), the per-chain min (MAX: max) of the input, which is
-// also the min (max) of the output.  Addends beyond the truncation are clamped
-// to wsT + 1: such a candidate already exceeds the cap g + wsT, clamped or not.
+// also the min (max) of the output.
 template <int LPL, bool PAD, int WIN, bool MAX = false>
-__device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], int ws_, int wsT_, int lane, int K, int& gA,
-                                            int& gB) {
+__device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], const DtK<LPL>& k, int& gA, int& gB) {
     const unsigned big = MAX ? kNegBigP : kBigP;
-    const int sg = MAX ? -1 : 1;
+    const int lane = k.lane;
     if constexpr (PAD) {
 #pragma unroll
         for (int e = 0; e < LPL; ++e)
-            if (lane * LPL + e >= K) x[e] = big;
+            if (lane * LPL + e >= k.K) x[e] = big;
     }
     unsigned lred = x[0];
 #pragma unroll
     for (int e = 1; e < LPL; ++e) lred = op2<MAX>(lred, x[e]);
     gA = MAX ? __reduce_max_sync(kFull, lo16(lred)) : __reduce_min_sync(kFull, lo16(lred));
     gB = MAX ? __reduce_max_sync(kFull, hi16(lred)) : __reduce_min_sync(kFull, hi16(lred));
-    const int clampv = wsT_ + 1;
+    const int clampv = k.wsT + 1;
     const unsigned G = pk(gA, gB);
-    const unsigned cap = __vadd2(G, pk(sg * wsT_, sg * wsT_));
-    const int ws1 = min(ws_, clampv);
-    const unsigned wsP = pk(sg * ws1, sg * ws1);
+    unsigned cap, wsP;
+    if constexpr (MAX) {
+        cap = __vsub2(G, k.capP);
+        wsP = __vsub2(0u, k.wsP);
+    } else {
+        cap = __vadd2(G, k.capP);
+        wsP = k.wsP;
+    }
     unsigned fw[LPL], bw[LPL];
     fw[0] = x[0];
 #pragma unroll
@@ -85,9 +115,10 @@ __device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], int ws_, int wsT
         inb = __shfl_down_sync(kFull, bw[0], 1);
     } else {
         unsigned cf = fw[LPL - 1], cb = bw[0];
+        const int sg = MAX ? -1 : 1;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const int st = min(ws_ * LPL * d, clampv);
+            const int st = min(k.ws * LPL * d, clampv);
             const unsigned stP = pk(sg * st, sg * st);
             const unsigned tf = __shfl_up_sync(kFull, cf, d);
             const unsigned tb = __shfl_down_sync(kFull, cb, d);
@@ -97,17 +128,14 @@ __device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], int ws_, int wsT
         inf = __shfl_up_sync(kFull, cf, 1);
         inb = __shfl_down_sync(kFull, cb, 1);
     }
-    // Lanes 0 / 31 have no left / right neighbour: the shuffle returned one of
-    // their own (real, >= min) values, so the addend wsT + 1 puts that candidate
-    // above the cap (no select needed).
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
         const bool needL = WIN > 0 ? (e + 1 < WIN) : true;
         const bool needR = WIN > 0 ? (LPL - e < WIN) : true;
-        const int al = lane == 0 ? clampv : min(ws_ * (e + 1), clampv);
-        const int ar = lane == 31 ? clampv : min(ws_ * (LPL - e), clampv);
-        const unsigned vf = needL ? addop2<MAX>(inf, pk(sg * al, sg * al), fw[e]) : fw[e];
-        const unsigned vb = needR ? addop2<MAX>(inb, pk(sg * ar, sg * ar), bw[e]) : bw[e];
+        const unsigned aL = MAX ? __vsub2(0u, k.aL[e]) : k.aL[e];
+        const unsigned aR = MAX ? __vsub2(0u, k.aR[e]) : k.aR[e];
+        const unsigned vf = needL ? addop2<MAX>(inf, aL, fw[e]) : fw[e];
+        const unsigned vb = needR ? addop2<MAX>(inb, aR, bw[e]) : bw[e];
         x[e] = op3_2<MAX>(vf, vb, cap);
     }
     return G;
@@ -127,9 +155,9 @@ struct MP {
 
 // Msg on a pair: x (packed, offsets oa/ob) -> normalised Msg output.
 template <int LPL, bool PAD, int WIN>
-__device__ __forceinline__ void msg2(unsigned (&x)[LPL], int& oa, int& ob, int ws, int wsT, int lane, int K) {
+__device__ __forceinline__ void msg2(unsigned (&x)[LPL], int& oa, int& ob, const DtK<LPL>& k) {
     int gA, gB;
-    const unsigned G = dtrans2<LPL, PAD, WIN, false>(x, ws, wsT, lane, K, gA, gB);
+    const unsigned G = dtrans2<LPL, PAD, WIN, false>(x, k, gA, gB);
 #pragma unroll
     for (int e = 0; e < LPL; ++e) x[e] = __vsub2(x[e], G);   // per half (values may be negative)
     oa += gA; ob += gB;
@@ -257,8 +285,7 @@ __device__ __forceinline__ unsigned sra1_2(unsigned z) {
 // (vj, bj*) = the node costs.  Out: pl = phi_ij, pr = phi_ji'.
 template <int LPL, bool PAD, int WIN>
 __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, int bib, const unsigned (&vj)[LPL],
-                                           int bja, int bjb, MP<LPL>& pl, MP<LPL>& pr, int ws, int wsT, int lane,
-                                           int K) {
+                                           int bja, int bjb, MP<LPL>& pl, MP<LPL>& pr, const DtK<LPL>& k) {
     // phi_ji := Msg(f_j + phi_{j+1,j})
     unsigned pji[LPL];
 #pragma unroll
@@ -266,7 +293,7 @@ __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, i
     const int ja = pr.a + bja, jb = pr.b + bjb;       // phi_ji left unnormalised
     {
         int g0, g1;
-        dtrans2<LPL, PAD, WIN, false>(pji, ws, wsT, lane, K, g0, g1);
+        dtrans2<LPL, PAD, WIN, false>(pji, k, g0, g1);
     }
     // t = floor((m_i - 2 phi_ji) / 2), m_i = phi_L + f_i + phi_ji; true offset C = pl.o + bi - pji.o
     const int ca = pl.a + bia - ja, cb = pl.b + bib - jb;
@@ -275,13 +302,13 @@ __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, i
 #pragma unroll
     for (int e = 0; e < LPL; ++e) t[e] = sra1_2(__vsub2(pl.m[e] + vi[e] + c0, pji[e]));
     int ta = ca >> 1, tb = cb >> 1;
-    msg2<LPL, PAD, WIN>(t, ta, tb, ws, wsT, lane, K);            // phi_ij
+    msg2<LPL, PAD, WIN>(t, ta, tb, k);                           // phi_ij
     // phi_ji' = Msg(-phi_ij) = -maxplus(phi_ij); normalised: gmax - maxplus(t_n)
     unsigned u[LPL];
 #pragma unroll
     for (int e = 0; e < LPL; ++e) u[e] = t[e];
     int gA, gB;
-    const unsigned Gm = dtrans2<LPL, PAD, WIN, true>(u, ws, wsT, lane, K, gA, gB);
+    const unsigned Gm = dtrans2<LPL, PAD, WIN, true>(u, k, gA, gB);
 #pragma unroll
     for (int e = 0; e < LPL; ++e) { pr.m[e] = __vsub2(Gm, u[e]); pl.m[e] = t[e]; }
     pr.a = -ta - gA; pr.b = -tb - gB;
