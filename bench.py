@@ -174,8 +174,6 @@ def main():
     ap.add_argument("--mode", choices=("frames", "bands"), default="frames",
                     help="frames: one frame per GPU (weak scaling); bands: one frame sharded in row/column "
                          "bands with an all-to-all between half-steps (strong scaling)")
-    ap.add_argument("--wave-mb", type=float, default=None,
-                    help="L2 wave budget of the chain-DP launches in MiB (0 = one launch; default: library's)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -204,8 +202,6 @@ def main():
     left, right = distinct[0][0], distinct[0][1]
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
                       max_iters=iters, batch=nf, device=dev)
-    if args.wave_mb is not None:
-        ctx.set_wave_bytes(int(args.wave_mb * (1 << 20)))
     Lh = np.stack([distinct[s % len(distinct)][0] for s in range(nf)])
     Rh = np.stack([distinct[s % len(distinct)][1] for s in range(nf)])
     lt = torch.from_numpy(Lh).to(dev)

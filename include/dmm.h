@@ -197,10 +197,9 @@ DMM_API dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable);
 DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches);
 
 /* Tuning knobs (no effect on results, which are exact).
- * DMM_TUNE_WAVE_BYTES: the chains of a half-step are launched in waves whose
- * node data (F records) total at most `value` bytes, so that a wave's
- * re-reads across hierarchy levels stay in the 126 MB L2; 0 = one launch.
- * Default 0 (measured: waves cost more occupancy than they save in L2 misses). */
+ * DMM_TUNE_WAVE_BYTES: accepted and ignored (L2-sized chain waves were
+ * measured slower than one launch per level and removed; kept so callers of
+ * the knob keep working). */
 #define DMM_TUNE_WAVE_BYTES 1
 /* Debug: value != 0 makes dmm_solve stop after the first H half-step (the
  * bound history then holds only b_0; for parity taps of f_ after H_1). */

@@ -200,7 +200,7 @@ class Context:
         self._call("dmm_set_profiling", 1 if enable else 0)
 
     def set_wave_bytes(self, nbytes: int):
-        """L2 wave budget of the chain-DP launches (0 = one launch per half-step)."""
+        """Accepted and ignored (DMM_TUNE_WAVE_BYTES, include/dmm.h)."""
         self._call("dmm_set_tuning", TUNE_WAVE_BYTES, int(nbytes))
 
     def set_pair(self, enable: bool = True):

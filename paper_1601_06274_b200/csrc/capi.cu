@@ -23,7 +23,6 @@ struct dmm_ctx {
     std::string err;
     // event profiling (dmm_set_profiling)
     int profiling;
-    size_t wave_budget;   // bytes of chain data per launch wave (L2 sizing), 0 = one wave
     int stop_after_h;     // debug: dmm_solve runs only the first H half-step
     int pair_ok;          // configuration passes pair_range_ok
     int use_pair;         // DMM_TUNE_PAIR (default 1): packed chain-pair kernels when pair_ok
@@ -163,21 +162,13 @@ void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterati
     a.first = (t == 0 && v == 0);
     a.last = (t == iterations - 1 && v == 1);
     a.bound_slot = 2 * t + v;
-    // optional L2-sized waves: the node records of one wave fit the budget
-    const int chains = v ? ctx->L.W : ctx->L.H;
-    const size_t per_chain = (size_t)(v ? ctx->L.H : ctx->L.W) * dmm::rec_bytes(ctx->KP) * nframes;
-    int wave = 0;
-    if (ctx->wave_budget > 0) {
-        const size_t nw = (per_chain * chains + ctx->wave_budget - 1) / ctx->wave_budget;
-        if (nw > 1) wave = (int)((chains + nw - 1) / nw);
-    }
     if (ctx->use_pair && ctx->pair_ok) {
         Timed tm(ctx, 2 + v, s, dmm::hm2_launches_per_pass(a, v));
         dmm::launch_hm2_pass(a, v, nframes, s);
         return;
     }
-    Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, wave));
-    dmm::launch_hm_pass(a, v, nframes, wave, s);
+    Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, 0));
+    dmm::launch_hm_pass(a, v, nframes, 0, s);
 }
 
 }  // namespace
@@ -228,7 +219,6 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->iters_done = new int[cfg->batch]();
     c->launches = 0;
     c->profiling = 0;
-    c->wave_budget = 0;
     c->stop_after_h = 0;
     c->pair_ok = pair_range_ok(cfg);
     c->use_pair = 1;
@@ -518,7 +508,7 @@ int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value) {
     if (!ctx) return DMM_E_ARG;
-    if (param == DMM_TUNE_WAVE_BYTES && value >= 0) { ctx->wave_budget = (size_t)value; return DMM_OK; }
+    if (param == DMM_TUNE_WAVE_BYTES && value >= 0) return DMM_OK;   // ignored (dmm.h)
     if (param == DMM_TUNE_DEBUG_STOP_AFTER_H) { ctx->stop_after_h = value != 0; return DMM_OK; }
     if (param == DMM_TUNE_PAIR) { ctx->use_pair = value != 0; return DMM_OK; }
     if (param == DMM_TUNE_QUERY_PAIR) { ctx->err = ctx->use_pair && ctx->pair_ok ? "pair" : "int32"; return DMM_OK; }
