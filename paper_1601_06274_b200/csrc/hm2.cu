@@ -251,15 +251,23 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
                     }
                 }
                 s += kCH;
-            } else {
+            } else {                     // partial chunk or spine node inside: per step, next decode ahead
                 const int cnt = ccount;
+                const int st = REV ? -kStride : kStride;
+                unsigned ra = base + (REV ? cnt - 1 : 0) * kStride;
+                unsigned v[LPL]; int ba, bb;
+                this->dec(ra, ra + kOffB, v, ba, bb);
 #pragma unroll 1
                 for (int k = 0; k < cnt; ++k) {
-                    unsigned v[LPL]; int ba, bb;
-                    const unsigned ra = base + (REV ? cnt - 1 - k : k) * kStride;
-                    this->dec(ra, ra + kOffB, v, ba, bb);
+                    unsigned vn[LPL]; int ban, bbn;
+                    ra += st;
+                    const unsigned rn = k + 1 < cnt ? ra : base;   // in-bounds dummy on the last step
+                    this->dec(rn, rn + kOffB, vn, ban, bbn);
                     step(v, ba, bb);
                     spine(s + k);
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) v[e] = vn[e];
+                    ba = ban; bb = bbn;
                 }
                 s += cnt;
             }
@@ -314,7 +322,7 @@ __global__ void __launch_bounds__(64) hm2_root_kernel(PassArgs a) {
 }
 
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int NW>
-__global__ void __launch_bounds__(NW * 32) hm2_level_kernel(PassArgs a, int lev, int ntasks) {
+__global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int lev, int ntasks) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
