@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(256) cost_kernel(Layout L, int frame0, int d_m
     __syncthreads();
     const int chunks = KP / 16;
     uint4* out = reinterpret_cast<uint4*>(P.D + (size_t)y * W * KP);
-    for (int q = threadIdx.x; q < W * chunks; q += blockDim.x) {
+    // blockIdx.y splits the row's output into gridDim.y contiguous parts
+    const int nq = W * chunks, per = (nq + gridDim.y - 1) / gridDim.y;
+    const int q0 = blockIdx.y * per, q1 = min(nq, q0 + per);
+    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
         const int x = q / chunks, k0 = (q % chunks) * 16;
         const uint32_t cl = sl[x];
         uint32_t w[4];
@@ -96,7 +99,7 @@ void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, c
     const size_t smem = 2 * (size_t)L.W * sizeof(uint32_t);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cost_kernel<<<dim3(L.H, 1, nframes), 256, smem, s>>>(L, frame0, d_min, oob);
+    cost_kernel<<<dim3(L.H, 4, nframes), 256, smem, s>>>(L, frame0, d_min, oob);
 }
 
 }  // namespace dmm
