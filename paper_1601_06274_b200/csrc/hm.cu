@@ -2,32 +2,31 @@
 // (H pass) or column (V pass) chain builds its hierarchical minorant
 // with Handshakes (Alg.5).
 //
-// Mapping:
-//  * one CTA per chain, NW warps; a warp owns one K-vector at a time with the
-//    label dimension in registers, LPL = KP/32 consecutive labels per lane;
-//    Msg / Handshake are the register-level primitives of hm_device.cuh.
+// One chain per warp in int32: the fallback of the packed chain-pair kernels
+// (hm2.cu) for configurations outside their 16-bit range check, and the
+// DMM_TUNE_PAIR = 0 path.  Mapping:
+//  * a warp owns one K-vector at a time with the label dimension in registers,
+//    LPL = KP/32 consecutive labels per lane; Msg / Handshake are the
+//    register-level primitives of hm_device.cuh.
 //  * node data F (the pass's unaries: D*2^F + g_ for H, f_ for V) are compact
 //    u16-span records (dmm_internal.cuh); they stream into a per-warp ring of
 //    kNSlot chunks x kCH nodes filled by TMA bulk copies (cp.async.bulk, one
-//    lane per node, one mbarrier per chunk).  The producer walks the warp's
-//    whole consumption order (RunSeq) and runs ahead across level barriers:
-//    node data never depend on the messages.
-//  * "global levels" (subchains longer than kCMax; hm_global_kernel, one CTA
-//    per chain): breadth first, one warp per subchain; only the message direction whose boundary changed is
-//    recomputed (Fig.11's dots are reused: "spine" messages a later level needs
-//    are kept in the fwd/bwd scratch arrays, L2-resident); each task's two
-//    message loads are issued one task ahead.
-//  * "leaf blocks" (the 2^l* subchains of length <= kCMax) run in a separate
-//    kernel with one warp per block (high occupancy: ~8 KB of shared memory
-//    per warp): TMA stages the block's records, D rows and its two boundary
-//    messages, and the warp finishes the sub-hierarchy on chip, depth first,
-//    the forward and backward passes of each piece interleaved (two
-//    independent Msg chains -> ILP), pending pieces on a compact-record stack.
-//    A leaf [p,p] with boundary messages L, R has lambda = L + F + R (reading
-//    R8); the pass writes L + R + D*2^F, which is f_ = lambda - g_ for H and
-//    D*2^F + g_ (the next H pass's unaries) for V, as a compact record.  Node
-//    minima of lambda sum to the dual bound (exactness); the last V pass
-//    writes the lowest-index argmin as the label (R13, R14).
+//    mbarrier per chunk); full chunks run unrolled with compile-time offsets.
+//  * level-synchronous launches: the root (level 0, two warps per chain: the
+//    forward and the backward pass, then the Handshake), the global levels
+//    1..l*-1 (one warp per (chain, subchain) task; only the message direction
+//    whose boundary changed is recomputed -- Fig.11's reuse: "spine" messages
+//    a later level needs go to the fwd/bwd scratch arrays), and the leaf blocks.
+//  * leaf blocks (the 2^l* subchains of length <= kCMax), one warp per block:
+//    TMA stages the block's records, D rows and its two boundary messages, and
+//    the warp finishes the sub-hierarchy on chip, depth first, the forward and
+//    backward passes of each piece interleaved (two independent Msg chains ->
+//    ILP), pending pieces on a compact-record stack.  A leaf [p,p] with
+//    boundary messages L, R has lambda = L + F + R (reading R8); the pass
+//    writes L + R + D*2^F, which is f_ = lambda - g_ for H and D*2^F + g_ (the
+//    next H pass's unaries) for V, as a compact record.  Node minima of lambda
+//    sum to the dual bound (exactness); the last V pass writes the
+//    lowest-index argmin as the label (R13, R14).
 // All arithmetic is exact int32 (ranges in DESIGN.md): bit-identical to the
 // CPU oracle whatever the evaluation order.
 #include "hm_device.cuh"
