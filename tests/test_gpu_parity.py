@@ -172,6 +172,25 @@ def test_errors():
         dmm.Context(width=16, height=8, d_min=0, d_max=300)   # K > 256
 
 
+@pytest.mark.parametrize("w,T,family", [(6, 3, "pair"), (6, 4, "int32")])
+def test_pair_range_edge(orc, w, T, family):
+    """At the edge of the packed 16-bit range check (w=6, T=3, F=4:
+    16*960 + 3*288 + 4 = 16228 <= 16383) the pair kernels still run and stay
+    exact; one step beyond (T=4) the int32 kernels take over."""
+    W, H, K, iters = 90, 31, 64, 3
+    left, right, _ = datagen.pair("rd", W, H, K, seed=77)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=w, T=T, frac_bits=4, max_iters=iters)
+    assert ctx.kernel_family() == family
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(iters)
+    e, b, hist = ctx.result()
+    o = _run_oracle(orc, left, right, 0, K, w, w, T, 4, iters)
+    assert np.array_equal(ctx.dual(0).cpu().numpy().astype(np.int64), o["fdual"])
+    assert np.array_equal(ctx.dual(1).cpu().numpy().astype(np.int64), o["gdual"])
+    assert np.array_equal(ctx.labels().cpu().numpy().astype(np.int32), o["labels"])
+    assert np.array_equal(np.array(hist), o["bound_hist"]) and e == o["energy"]
+
+
 def test_frame_stack_apis(orc):
     """dmm_cost_volume_frames + dmm_solve(nframes) and dmm_run_host_frames
     (configs[4]-style streams) equal the oracle frame by frame."""
