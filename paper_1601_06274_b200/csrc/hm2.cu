@@ -29,6 +29,17 @@ static_assert(kRootCH <= 16 && kLevCH <= 16, "pair_range_ok (capi.cu) allows 16 
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
 
+// Programmatic dependent launch: the kernels of a half-step are launched with
+// programmatic stream serialisation, so a kernel's prologue (ring / mbarrier
+// setup and the TMA staging of the pass's node records, which were written
+// before the half-step's root started) overlaps the tail of the previous
+// level.  Everything that reads or writes the previous level's outputs (the
+// spine scratch, bounds, labels, output records) comes after pdl_wait(),
+// which returns once the previous kernel has completed and its writes are
+// visible; pdl_trigger() lets the next kernel start its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void task_bounds(int n, int lev, int s, int& lo, int& hi) {
     lo = 0; hi = n - 1;
     for (int b = lev - 1; b >= 0; --b) {
@@ -297,6 +308,8 @@ __global__ void __launch_bounds__(64) hm2_root_kernel(PassArgs a) {
     h.init(a, lane);
     h.set_pair(blockIdx.x);
     h.ring_init(smem + warp * lay.total, lay);
+    pdl_wait();          // the node records were written by the previous half-step
+    pdl_trigger();
     const int n = h.n, i = n / 2 - 1, j = i + 1;
     MP<LPL> zero, phi;
     zero.zero(); phi.zero();
@@ -331,6 +344,7 @@ __global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int 
     h.init(a, lane);
     h.ring_init(smem + warp * lay.total, lay);
     const int n = h.n;
+    bool waited = false;
 #pragma unroll 1
     for (int t = blockIdx.x * NW + warp; t < ntasks; t += gridDim.x * NW) {
         h.set_pair(t >> lev);
@@ -343,6 +357,7 @@ __global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int 
             h.rs0 = hi; h.rd0 = -1; h.rc0 = hi - j;
             h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
             h.start(2);
+            if (!waited) { pdl_wait(); pdl_trigger(); waited = true; }
             h.ld_spine(false, hi, bnd);
             h.ld_spine(true, ii, spn);
             h.template run_pass<-1>(hi, hi - j, bnd);
@@ -351,12 +366,14 @@ __global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int 
             h.rs0 = lo; h.rd0 = 1; h.rc0 = ii - lo;
             h.rs1 = j; h.rd1 = -1; h.rc1 = 2;
             h.start(2);
+            if (!waited) { pdl_wait(); pdl_trigger(); waited = true; }
             h.ld_spine(true, lo, bnd);
             h.ld_spine(false, j, spn);
             h.template run_pass<1>(lo, ii - lo, bnd);
             h.handshake(ii, bnd, spn);
         }
     }
+    if (!waited) { pdl_wait(); pdl_trigger(); }
 }
 
 // ============================================================== leaf kernel
@@ -462,6 +479,12 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
     PS h;
     h.init(a, lane);
     const int n = h.n;
+    bool waited = false;
+    if (lstar == 0) {       // no root before this kernel: its records come from the previous kernel
+        pdl_wait();
+        pdl_trigger();
+        waited = true;
+    }
 
 #pragma unroll 1
     for (int b = blockIdx.x * kNWL + warp; b < nblocks; b += gridDim.x * kNWL) {
@@ -494,6 +517,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
                 }
             }
         }
+        if (!waited) { pdl_wait(); pdl_trigger(); waited = true; }
         MP<LPL> L, R, Kp;
         // Fig.11 reuse for the block's first split: a left block keeps its left
         // boundary, so the message into its split node from the left is on the
@@ -623,6 +647,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         }
         __syncwarp();
     }
+    if (!waited) pdl_wait();
     if (lane == 0 && bsum != 0)
         atomicAdd(reinterpret_cast<unsigned long long*>(&h.P.bounds[a.bound_slot]), (unsigned long long)bsum);
 }
@@ -632,6 +657,22 @@ static int leaf_level(int n) {
     int l = 0;
     while (((n + (1 << l) - 1) >> l) > kCMax) ++l;
     return l;
+}
+
+// Launch with programmatic stream serialisation (see pdl_wait / pdl_trigger).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
 // Per-instantiation launch constants (SM count, occupancy, smem opt-in),
@@ -672,18 +713,18 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
         lc.dev = dev;
     }
     if (lstar > 0) {
-        rk<<<dim3(units, nframes), 64, 2 * rr, s>>>(a);
+        launch_pdl(rk, dim3(units, nframes), 64, 2 * rr, s, a);
         for (int lev = 1; lev < lstar; ++lev) {
             const int ntasks = units << lev;
             int grid = (ntasks + kNWG - 1) / kNWG;
             if (grid > lc.lev_cap) grid = lc.lev_cap;
-            lk<<<dim3(grid, nframes), kNWG * 32, kNWG * rs, s>>>(a, lev, ntasks);
+            launch_pdl(lk, dim3(grid, nframes), kNWG * 32, kNWG * rs, s, a, lev, ntasks);
         }
     }
     const int nblocks = units << lstar;
     int grid = (nblocks + kNWL - 1) / kNWL;
     if (grid > lc.leaf_cap) grid = lc.leaf_cap;
-    kern<<<dim3(grid, nframes), kNWL * 32, smem, s>>>(a, lstar, nblocks);
+    launch_pdl(kern, dim3(grid, nframes), kNWL * 32, smem, s, a, lstar, nblocks);
 }
 
 template <int LPL, bool PAD, int WIN>
