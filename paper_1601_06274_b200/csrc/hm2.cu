@@ -660,8 +660,11 @@ static int leaf_level(int n) {
 }
 
 // Launch with programmatic stream serialisation (see pdl_wait / pdl_trigger).
+// Used for LPL <= 4 only: with the large K = 256 footprints (C3) the early
+// dependent CTAs cost more than the overlap gains (measured 81 -> 74 fps).
 template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+static void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -671,7 +674,7 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -713,18 +716,18 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
         lc.dev = dev;
     }
     if (lstar > 0) {
-        launch_pdl(rk, dim3(units, nframes), 64, 2 * rr, s, a);
+        launch_pdl(LPL <= 4, rk, dim3(units, nframes), 64, 2 * rr, s, a);
         for (int lev = 1; lev < lstar; ++lev) {
             const int ntasks = units << lev;
             int grid = (ntasks + kNWG - 1) / kNWG;
             if (grid > lc.lev_cap) grid = lc.lev_cap;
-            launch_pdl(lk, dim3(grid, nframes), kNWG * 32, kNWG * rs, s, a, lev, ntasks);
+            launch_pdl(LPL <= 4, lk, dim3(grid, nframes), kNWG * 32, kNWG * rs, s, a, lev, ntasks);
         }
     }
     const int nblocks = units << lstar;
     int grid = (nblocks + kNWL - 1) / kNWL;
     if (grid > lc.leaf_cap) grid = lc.leaf_cap;
-    launch_pdl(kern, dim3(grid, nframes), kNWL * 32, smem, s, a, lstar, nblocks);
+    launch_pdl(LPL <= 4, kern, dim3(grid, nframes), kNWL * 32, smem, s, a, lstar, nblocks);
 }
 
 template <int LPL, bool PAD, int WIN>
