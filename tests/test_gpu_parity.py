@@ -88,6 +88,11 @@ CASES = [
     (1025, 3, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),       # long rows, odd splits
     (5, 513, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),        # long columns
     (1500, 24, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),   # C3 row length and K
+    # C3's K = 256 with tall columns: the V level kernels (LPL = 8) run at
+    # levels >= 1 (leaf level 7 at H = 1000, 6 at H = 700)
+    (7, 1000, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),
+    (9, 700, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),
+    (33, 1000, 200, 0, 2, 3, 3, 4, 2, 2, "wt-middlebury"),   # padded K = 200 -> 256, odd W (self-paired chain)
 ]
 
 
@@ -141,6 +146,35 @@ def test_run_host_matches_device_path(orc):
     o = _run_oracle(orc, l, r, 0, K, 3, 3, 4, 4, 4)
     assert np.array_equal(lab.numpy().astype(np.int32), o["labels"])
     assert e == o["energy"] and b == o["bound_hist"][-1]
+
+
+@pytest.mark.parametrize("orient", ["row", "column"])
+def test_hm_golden_chains_gpu(orient):
+    """tests/golden/hm_chains.json (n = 7, 13, 25; F = 0, 4; oracle-written,
+    pinned in test_oracle_chain.py) through the device path: a 1-row frame's
+    f_ after H_1 is HM(D*2^F) (g_ = 0, R4); a 1-column frame's g_ after V_1 is
+    HM(D*2^F) - D*2^F (the H pass of single nodes gives f_ = D*2^F)."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "hm_chains.json")) as f:
+        g = json.load(f)
+    for c in g["chains"]:
+        n, Fb = c["n"], c["F"]
+        D = np.array(c["D"], np.uint8)
+        lam = np.array(c["lam"], np.int64)
+        W, H = (n, 1) if orient == "row" else (1, n)
+        ctx = _ctx(width=W, height=H, d_min=0, d_max=g["K"] - 1, w=g["w"], T=g["T"], frac_bits=Fb, max_iters=1)
+        ctx.import_cost_volume(torch.from_numpy(D.reshape(H, W, g["K"])).cuda())
+        ctx.solve(1)
+        e, b, hist = ctx.result()
+        if orient == "row":
+            got = ctx.dual(0).cpu().numpy().reshape(n, -1).astype(np.int64)
+            assert np.array_equal(got, lam), (n, Fb)
+            assert hist[0] == c["opt"]
+        else:
+            got = ctx.dual(1).cpu().numpy().reshape(n, -1).astype(np.int64)
+            assert np.array_equal(got, lam - (D.astype(np.int64) << Fb)), (n, Fb)
+            assert hist[1] == c["opt"]
 
 
 def test_deterministic_repeat():
@@ -222,6 +256,46 @@ def test_c2_full_size(orc):
     g = _run_gpu(left, right, *args)
     o = _run_oracle(orc, left, right, *args, nthreads=max(1, min(16, __import__("os").cpu_count() or 1)))
     _compare(g, o)
+
+
+@pytest.mark.slow
+def test_c3_full_size(orc):
+    """configs[2] at full size on one GPU (1500x1000x256, 4 iterations, the
+    launch configuration bench.py --config C3 times): complete element-by-
+    element comparison of codes, D, f_, g_, labels, bound history, energy."""
+    import os
+    c = datagen.CONFIGS["C3"]
+    left, right, _ = datagen.pair(c["kind"], c["W"], c["H"], c["K"], 0)
+    args = (c["d_min"], c["K"], 3, 3, 4, 4, c["iters"])
+    g = _run_gpu(left, right, *args)
+    o = _run_oracle(orc, left, right, *args, nthreads=max(1, os.cpu_count() or 1))
+    _compare(g, o)
+
+
+@pytest.mark.slow
+def test_c2_full_size_deterministic_records():
+    """Ten full C2 solves (bench launch configuration) produce byte-identical
+    dual records (f_ and D*2^F + g_, the whole workspace arrays the kernels
+    write, pads excluded), labels and bound histories: no race between the
+    level / leaf kernels, PDL prologues and the TMA staging."""
+    import paper_1601_06274_b200 as dmm
+    c = datagen.CONFIGS["C2"]
+    left, right, _ = datagen.pair(c["kind"], c["W"], c["H"], c["K"], 0)
+    ctx = _ctx(width=c["W"], height=c["H"], d_min=0, d_max=c["K"] - 1, w=3, T=4, frac_bits=4,
+               max_iters=c["iters"])
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    ref = None
+    nb = 2 * 128 + 4                      # u16 spans + int32 base of each record
+    for _ in range(10):
+        ctx.cost_volume(lt, rt)
+        ctx.solve(c["iters"])
+        cur = (ctx.buffer(dmm.BUF_FV)[:, :, :nb].clone(), ctx.buffer(dmm.BUF_FH)[:, :, :nb].clone(),
+               ctx.labels(), ctx.result())
+        if ref is None:
+            ref = cur
+        else:
+            assert torch.equal(cur[0], ref[0]) and torch.equal(cur[1], ref[1])
+            assert torch.equal(cur[2], ref[2]) and cur[3] == ref[3]
 
 
 # ---------------------------------------------------------------- primitives

@@ -179,3 +179,80 @@ def test_hm_long_chain_exact(orc):
         # maximality via DP min-marginals of F - lam (dp itself pinned above)
         mm = orc.min_marginals(F - lam, ws, T)
         assert np.all(mm == 0)
+
+
+# ------------------------------------- HM rounding / split pins (R7, R9)
+def _split_tree_check(lam, lo, hi, opt):
+    """Every piece [lo, hi] of the recursion (R5, left part floor(len/2), R7)
+    whose optimum is `opt` hands ceil(opt/2) to its left part and floor(opt/2)
+    to its right part: the Handshake splits the min-marginal m_i with floor
+    halving (Alg.5 line 3, reading R9), so the right part receives
+    min floor((m_i - 2 phi_ji)/2) + min phi_ji = floor(opt/2), and exactness of
+    the whole minorant leaves the rest to the left part.  A piece's optimum is
+    the sum of its nodes' minima (exactness, recursively)."""
+    piece = lam[lo:hi + 1].min(1).sum()
+    assert piece == opt, (lo, hi, piece, opt)
+    if lo == hi:
+        return
+    i = lo + (hi - lo + 1) // 2 - 1
+    _split_tree_check(lam, lo, i, -(-opt // 2))
+    _split_tree_check(lam, i + 1, hi, opt // 2)
+
+
+def test_hm_recursive_optimum_split(orc):
+    """Pins R7 (split point) and R9 (floor halving) at every level of the
+    recursion: a ceil-halving or ceil-split variant fails on odd optima / odd
+    lengths.  The chain optimum comes from the plain Viterbi (never calls HM)."""
+    rng = np.random.default_rng(21)
+    for _ in range(600):
+        n = int(rng.integers(1, 70)); K = int(rng.integers(1, 7))
+        ws = int(rng.integers(0, 40)); T = int(rng.integers(1, K + 2))
+        F = rng.integers(-50, 200, size=(n, K))
+        lam = orc.hm(F, ws, T)
+        _split_tree_check(lam, 0, n - 1, orc.chain_min(F, ws, T)[0])
+
+
+def _hm_chains():
+    with open(os.path.join(GOLD, "hm_chains.json")) as f:
+        return json.load(f)
+
+
+def test_hm_golden_chains(orc):
+    """Odd-length and deeper chains (n = 7, 13, 25; F = 0, 4) of
+    tests/golden/hm_chains.json: the stored values satisfy the independent pins
+    (Viterbi optimum, recursive optimum split, maximality via DP min-marginals,
+    brute-force minorant on n = 7) and the oracle reproduces them."""
+    g = _hm_chains()
+    ws0, T = g["w"], g["T"]
+    for c in g["chains"]:
+        D = np.array(c["D"], np.int64) << c["F"]
+        lam = np.array(c["lam"], np.int64)
+        ws = ws0 << c["F"]
+        v, _ = orc.chain_min(D, ws, T)
+        assert v == c["opt"]
+        _split_tree_check(lam, 0, c["n"] - 1, v)
+        assert np.all(orc.min_marginals(D - lam, ws, T) == 0)
+        if c["n"] == 7:
+            _check_minorant(D, ws, T, lam)
+        assert np.array_equal(orc.hm(D, ws, T), lam)
+
+
+def test_hm_golden_hand_check(orc):
+    """The hand-worked first Handshake of chains[0] (Alg.5 lines 1-4 with the
+    O(K^2) Msg definition): its messages agree with the brute-force Msg and the
+    stored lambda's top-level split matches the hand-computed optima."""
+    g = _hm_chains()
+    h = g["_hand_check"]
+    c = g["chains"][0]
+    D = np.array(c["D"], np.int64)
+    ws, T = g["w"], g["T"]
+    assert np.array_equal(orc.msg(np.array(h["alg5_line3_floor_half_m_i_minus_2phi_ji"]), ws, T, direct=True),
+                          h["alg5_line3_phi_ij"])
+    assert np.array_equal(orc.msg(-np.array(h["alg5_line3_phi_ij"]), ws, T, direct=True),
+                          h["alg5_line4_phi_ji_bounced"])
+    assert np.array_equal(orc.msg(D[3] + np.array(h["phi_into_j_from_right"]), ws, T, direct=True),
+                          h["alg5_line1_phi_ji"])
+    lam = np.array(c["lam"])
+    assert lam[:3].min(1).sum() == h["left_part_optimum"] and lam[3:].min(1).sum() == h["right_part_optimum"]
+    # leaves of the left part see phi_ji' at node i = 2 as their right boundary
+    assert min(np.array(h["alg5_line2_m_i"])) == h["chain_optimum"] == c["opt"]
