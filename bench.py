@@ -42,15 +42,45 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def traffic_per_half_step():
+def traffic_per_half_step(config):
     """dram__bytes_read.sum + dram__bytes_write.sum of one chain-DP half-step
-    (its root + level + leaf launches) from the committed ncu capture summary
-    (profiles/ncu_traffic.json, written by the launch-list capture), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    (its root + level + leaf launches, averaged over the H and V half-steps of
+    one solve) from the committed ncu capture OF THIS CONFIG
+    (profiles/ncu_traffic_<config>.json, written by profiles/summarize_ncu.py
+    from the launch-list capture), or None when no capture of this config exists."""
+    p = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("hm_bytes_per_half_step")
+            d = json.load(f)
+        if d.get("config") == config:
+            return d.get("hm_bytes_per_half_step")
     return None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def alg_bytes_compact(W, H, K, iters, frames=1):
+    """SURVEY 8(d) algorithmic bytes of the chain-DP half-steps of one step, on
+    the lossless compact basis (u16 label spans + one int32 offset per pixel
+    and vector; each input read once, each output written once, messages on
+    chip): H_1 = D (1) + f_ (2) B/cell + 4 B/pixel; H_t = D (1) + g_ (2) + f_ (2)
+    B/cell + 8 B/pixel; V = f_ (2) + g_ (2) B/cell + 8 B/pixel, + 1 B/pixel of
+    labels on the last V.  Cells = W*H*K (the padding to KP is not
+    algorithmic; the V pass's D re-read is traffic, not algorithmic bytes)."""
+    cells, px = W * H * K, W * H
+    h1 = 3 * cells + 4 * px
+    ht = 5 * cells + 8 * px
+    v = 4 * cells + 8 * px
+    return frames * (h1 + (iters - 1) * ht + iters * v + px)
 
 
 class ClockSampler:
@@ -154,7 +184,8 @@ def run_reference(args):
         "config": {"workload": f"{args.config}: stereo {W}x{H}, {K} disparities, census 5x5, {iters} dual iterations "
                                f"(reference arm: bounded sample of the first {rows} rows per step)",
                    "W": W, "H": H, "K": K, "iters": iters, "sample_rows": rows},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -222,8 +253,7 @@ def main():
     # outside the timed events; the step's own working set (~1.0 GB) exceeds L2.
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    ctx.read_profile()
-    ctx.set_profiling(True)
+    ctx.set_profiling(False)     # the headline steps run exactly as a user's calls (no per-kernel events)
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
@@ -241,8 +271,6 @@ def main():
         dist.barrier()
     launches = ctx.launch_count - launches0
     clocks = sampler.stop()
-    ctx.set_profiling(False)
-    prof = ctx.read_profile()
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     e, b, hist = ctx.result()
     if world > 1:
@@ -250,34 +278,43 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
+    # per-kernel-class timings from a separate profiled pass (CUDA events
+    # around every half-step on the launching stream, same L2 flush)
+    prof_steps = max(1, min(args.steps, 50))
+    ctx.read_profile()
+    ctx.set_profiling(True)
+    for i in range(prof_steps):
+        flush.fill_(i & 0xff)
+        step()
+    torch.cuda.synchronize(dev)
+    ctx.set_profiling(False)
+    prof = ctx.read_profile()
+
     cells = W * H * K
     value = world * nf * cells * iters / (ms / 1e3)
 
     # roofline of the dominant kernel: the chain-DP half-step (root + level +
-    # leaf launches of hm2.cu / hm.cu), H and V; one "launch" = one half-step
+    # leaf launches, H and V); one "launch" = one half-step.  Achieved =
+    # SURVEY 8(d) compact algorithmic bytes / the measured half-step time.
     hbm, peak_kind = peaks()
     ms_h, n_h = prof["hm_h"]
     ms_v, n_v = prof["hm_v"]
-    # compact dual records (u16 spans + int32 base,
-    # REC = 2*KP + 16 bytes per pixel) and the u8 cost volume, each input read
-    # once and each output written once per half-step:
-    #   H_1: D + f_ rec;  H_t: (D*2^F + g_) rec + D + f_ rec;  V: f_ rec + D + (D*2^F + g_) rec
-    KP = 32 * max(1, (K + 31) // 32)
-    while KP < K:
-        KP *= 2
-    rec = (2 * KP + 16) * W * H
-    dbytes = KP * W * H
-    alg_bytes_per_step = nf * ((dbytes + rec) + (iters - 1) * (2 * rec + dbytes) + iters * (2 * rec + dbytes))
-    achieved = alg_bytes_per_step * args.steps / ((ms_h + ms_v) / 1e3) / 1e9
-    tr = traffic_per_half_step()
-    step_ms_prof = sum(v[0] for v in prof.values()) / args.steps
+    alg_bytes_per_step = alg_bytes_compact(W, H, K, iters, nf)
+    hm_ms_per_step = (ms_h + ms_v) / prof_steps
+    achieved = alg_bytes_per_step / (hm_ms_per_step / 1e3) / 1e9
+    tr = traffic_per_half_step(args.config)
+    step_ms_prof = sum(v[0] for v in prof.values()) / prof_steps
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": tr, "kernel": "chain-DP half-step (root+level+leaf kernels), H and V",
-                "peak_kind": peak_kind, "launches": n_h + n_v, "half_steps": 2 * iters * args.steps,
+                "basis": "SURVEY 8(d) compact: H_1 3, H_t 5, V 4 B/cell + int32 offsets 4/8/8 B/pixel "
+                         "+ 1 B/pixel labels; achieved = bytes / CUDA-event half-step time",
+                "peak_kind": peak_kind, "half_steps_per_step": 2 * iters * nf,
+                "hm_ms_per_step": hm_ms_per_step, "profiled_steps": prof_steps,
                 "kernel_family": ctx.kernel_family(),
-                "alg_bytes_per_half_step": alg_bytes_per_step / (2 * iters),
-                "share_of_step": (ms_h + ms_v) / args.steps / step_ms_prof if step_ms_prof else None,
-                "per_class_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()}}
+                "alg_bytes_per_half_step": alg_bytes_per_step / (2 * iters * nf),
+                "traffic_source": f"profiles/ncu_traffic_{args.config}.json" if tr else None,
+                "share_of_step": hm_ms_per_step / step_ms_prof if step_ms_prof else None,
+                "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
 
     # end to end through the public C ABI with host buffers
     e2e = None
@@ -319,8 +356,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nth = os.cpu_count() or 1
-        v, dt, desc = cpu_oracle_sample(left, right, K, 2, nth)
-        cpu = {"value": v, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc, "seconds": dt}
+        v, dt, desc = cpu_oracle_sample(left, right, K, iters, nth)
+        cpu = {"value": v, "unit": UNIT, "cores": nth, "kind": "oracle", "sample": desc, "seconds": dt,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {

@@ -17,6 +17,8 @@
  *    host pointers are ordinary (preferably pinned) host memory.
  *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
  *    Every call is stream-ordered and asynchronous unless it says "synchronises".
+ *  - Every entry point taking a context runs on the context's device and
+ *    restores the caller's current CUDA device before returning.
  *  - Ownership: the caller owns images, outputs and the device workspace
  *    (allocate with dmm_workspace_bytes()); the context owns only small host
  *    state.  A context is single-threaded; distinct contexts are independent.
@@ -27,6 +29,7 @@
  *  - Errors: DMM_E_ARG invalid argument / config, DMM_E_SHAPE pitch < width,
  *    DMM_E_STATE solve before cost volume / result before solve,
  *    DMM_E_CUDA a CUDA runtime error (text in dmm_last_error()),
+ *    DMM_E_NCCL an NCCL error of a sharded context (dmm_shard),
  *    DMM_E_RANGE config outside the exact compact-storage range (dmm_create).
  */
 #ifndef DMM_B200_H
@@ -49,11 +52,12 @@ typedef enum {
     DMM_E_SHAPE = 2,
     DMM_E_STATE = 3,
     DMM_E_CUDA = 4,
+    DMM_E_NCCL = 5,
     DMM_E_RANGE = 6
 } dmm_status;
 
 typedef struct dmm_config {
-    int32_t width, height;   /* >= 1 each; the grid of P:145-152 (4-connected)        */
+    int32_t width, height;   /* 1..16384 each; the grid of P:145-152 (4-connected)      */
     int32_t d_min, d_max;    /* disparity range; K = d_max - d_min + 1 in [1, 256]       */
     int32_t census_radius;   /* 1 (3x3, 8 bits) or 2 (5x5, 24 bits), R17         */
     int32_t w_h, w_v;        /* pairwise weights >= 0: f_ij = w * min(|a-b|, trunc)      */
@@ -171,7 +175,12 @@ DMM_API dmm_status dmm_handshake(const int32_t* Fi, const int32_t* Fj, const int
  * and accumulated.  The V half-step reads the FV records, the H half-step
  * (t > 0) the FH records, so a caller may exchange those between half-steps.
  * dmm_energy: primal energy (Eq.3, scaled by 2^F) of the frame's current
- * labels; synchronises `stream` and writes *energy. */
+ * labels; synchronises `stream` and writes *energy.
+ * dmm_energy_of: the same energy of an arbitrary labelling `labels` (device
+ * u8 [H][W] label indices, disparity = d_min + label
+ * energy_evaluate) against the frame's cost volume; DMM_E_STATE before the
+ * cost volume, DMM_E_ARG if a label is >= K (checked on the device).
+ * Synchronises `stream`. */
 #define DMM_BUF_D 0
 #define DMM_BUF_FV 1
 #define DMM_BUF_FH 2
@@ -183,6 +192,7 @@ DMM_API dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t
 DMM_API dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int vertical,
                                  int32_t iterations, void* stream);
 DMM_API dmm_status dmm_energy(dmm_ctx* ctx, int frame, int64_t* energy, void* stream);
+DMM_API dmm_status dmm_energy_of(dmm_ctx* ctx, int frame, const uint8_t* labels, int64_t* energy, void* stream);
 
 /* Number of kernels this context has launched since creation. */
 DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
@@ -197,12 +207,10 @@ DMM_API dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable);
 DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches);
 
 /* Tuning knobs (no effect on results, which are exact).
- * DMM_TUNE_WAVE_BYTES: accepted and ignored (L2-sized chain waves were
- * measured slower than one launch per level and removed; kept so callers of
- * the knob keep working). */
-#define DMM_TUNE_WAVE_BYTES 1
-/* Debug: value != 0 makes dmm_solve stop after the first H half-step (the
- * bound history then holds only b_0; for parity taps of f_ after H_1). */
+ * DMM_TUNE_DEBUG_STOP_AFTER_H (debug): value != 0 makes dmm_solve stop after
+ * the first H half-step, for the parity tap of f_ after H_1 (dmm_copy_dual
+ * which = 0).  Such a partial solve computes no energy and no labelling:
+ * dmm_result, dmm_copy_labels and dmm_copy_dual(which = 1) return DMM_E_STATE. */
 #define DMM_TUNE_DEBUG_STOP_AFTER_H 2
 /* DMM_TUNE_PAIR: value != 0 (default) runs the half-steps on chain pairs in
  * packed 16-bit arithmetic (two chains per warp) whenever the configuration

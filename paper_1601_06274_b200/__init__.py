@@ -27,10 +27,10 @@ EXPORTS = (
     "dmm_run_host", "dmm_launch_count", "dmm_status_str", "dmm_last_error",
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
-    "dmm_cost_volume_frames", "dmm_run_host_frames",
+    "dmm_cost_volume_frames", "dmm_run_host_frames", "dmm_energy_of",
 )
 BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
-TUNE_WAVE_BYTES = 1
+TUNE_STOP_AFTER_H = 2
 TUNE_PAIR = 3
 TUNE_QUERY_PAIR = 4
 PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
@@ -88,6 +88,7 @@ def load_library():
         "dmm_import_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P]),
         "dmm_half_step": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, i32, ctypes.c_int, i32, P]),
         "dmm_energy": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(i64), P]),
+        "dmm_energy_of": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.POINTER(i64), P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -102,9 +103,9 @@ def torch_int64():
     return torch.int64
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device=None) -> int:
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return s.cuda_stream
 
 
@@ -199,9 +200,9 @@ class Context:
         """Record CUDA events around every kernel launch (on its stream)."""
         self._call("dmm_set_profiling", 1 if enable else 0)
 
-    def set_wave_bytes(self, nbytes: int):
-        """Accepted and ignored (DMM_TUNE_WAVE_BYTES, include/dmm.h)."""
-        self._call("dmm_set_tuning", TUNE_WAVE_BYTES, int(nbytes))
+    def set_stop_after_h(self, enable: bool = True):
+        """Debug: the next solve stops after the first H half-step (f_ tap only)."""
+        self._call("dmm_set_tuning", TUNE_STOP_AFTER_H, 1 if enable else 0)
 
     def set_pair(self, enable: bool = True):
         """Chain-pair packed 16-bit kernels (default on; used only when the
@@ -232,7 +233,7 @@ class Context:
         if left.stride(0) != right.stride(0):
             raise DmmError("left/right row pitch differ")
         self._call("dmm_cost_volume", frame, ctypes.c_void_p(left.data_ptr()),
-                   ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream))
+                   ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream, self.device))
 
     def cost_volume_frames(self, left, right, frame: int = 0, stream=None):
         """left/right: torch.uint8 (nframes, H, W) contiguous stacks on this device:
@@ -244,10 +245,10 @@ class Context:
         if left.shape[0] != right.shape[0]:
             raise DmmError("left/right frame counts differ")
         self._call("dmm_cost_volume_frames", frame, int(left.shape[0]), ctypes.c_void_p(left.data_ptr()),
-                   ctypes.c_void_p(right.data_ptr()), self.W, _stream_handle(stream))
+                   ctypes.c_void_p(right.data_ptr()), self.W, _stream_handle(stream, self.device))
 
     def solve(self, iterations: int = 4, frame: int = 0, nframes: int = 1, stream=None):
-        self._call("dmm_solve", frame, nframes, iterations, _stream_handle(stream))
+        self._call("dmm_solve", frame, nframes, iterations, _stream_handle(stream, self.device))
         for f in range(frame, frame + nframes):
             self._iters[f] = iterations
 
@@ -257,32 +258,32 @@ class Context:
         e = ctypes.c_int64()
         b = ctypes.c_int64()
         hist = (ctypes.c_int64 * max(2 * it, 1))()
-        self._call("dmm_result", frame, ctypes.byref(e), ctypes.byref(b), hist, _stream_handle(stream))
+        self._call("dmm_result", frame, ctypes.byref(e), ctypes.byref(b), hist, _stream_handle(stream, self.device))
         return int(e.value), int(b.value), [int(v) for v in hist[: 2 * it]]
 
     def labels(self, frame: int = 0, stream=None):
         import torch
         out = torch.empty((self.H, self.W), dtype=torch.uint8, device=self.device)
-        self._call("dmm_copy_labels", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        self._call("dmm_copy_labels", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream, self.device))
         return out
 
     def codes(self, which: int, frame: int = 0, stream=None):
         import torch
         out = torch.empty((self.H, self.W), dtype=torch.int32, device=self.device)
-        self._call("dmm_copy_codes", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        self._call("dmm_copy_codes", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream, self.device))
         return out
 
     def cost_volume_tensor(self, frame: int = 0, stream=None):
         import torch
         out = torch.empty((self.H, self.W, self.K), dtype=torch.uint8, device=self.device)
-        self._call("dmm_copy_cost_volume", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        self._call("dmm_copy_cost_volume", frame, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream, self.device))
         return out
 
     def dual(self, which: int, frame: int = 0, stream=None):
         """which 0: f_ after the last H half-step; 1: g_ after the last V half-step."""
         import torch
         out = torch.empty((self.H, self.W, self.K), dtype=torch.int32, device=self.device)
-        self._call("dmm_copy_dual", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream))
+        self._call("dmm_copy_dual", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream, self.device))
         return out
 
     # ------------------------------------------------ sharding building blocks
@@ -304,12 +305,12 @@ class Context:
         D = D.contiguous()
         if tuple(D.shape) != (self.H, self.W, self.K):
             raise DmmError(f"cost volume shape {tuple(D.shape)} != {(self.H, self.W, self.K)}")
-        self._call("dmm_import_cost_volume", frame, ctypes.c_void_p(D.data_ptr()), _stream_handle(stream))
+        self._call("dmm_import_cost_volume", frame, ctypes.c_void_p(D.data_ptr()), _stream_handle(stream, self.device))
         self._iters[frame] = 0
 
     def half_step(self, t: int, vertical: int, iterations: int, frame: int = 0, nframes: int = 1, stream=None):
         """One half-step of Algorithm 2 (H if vertical == 0, else V) of iteration t."""
-        self._call("dmm_half_step", frame, nframes, t, vertical, iterations, _stream_handle(stream))
+        self._call("dmm_half_step", frame, nframes, t, vertical, iterations, _stream_handle(stream, self.device))
         if vertical and t == iterations - 1:
             for f in range(frame, frame + nframes):
                 self._iters[f] = iterations
@@ -318,10 +319,19 @@ class Context:
         """int64 CUDA tensor view of the frame's bound history slots."""
         return self.buffer(BUF_BOUNDS, frame)
 
-    def energy(self, frame: int = 0, stream=None) -> int:
-        """Primal energy (scaled by 2**frac_bits) of the frame's current labels (synchronises)."""
+    def energy(self, frame: int = 0, stream=None, labels=None) -> int:
+        """Primal energy (Eq.3, scaled by 2**frac_bits) of the frame's
+        current labels, or of `labels` (uint8 (H, W) label indices on this
+        device) against the frame's cost volume.  Synchronises."""
         e = ctypes.c_int64()
-        self._call("dmm_energy", frame, ctypes.byref(e), _stream_handle(stream))
+        if labels is None:
+            self._call("dmm_energy", frame, ctypes.byref(e), _stream_handle(stream, self.device))
+        else:
+            if (labels.dtype.itemsize != 1 or labels.device != self.device or tuple(labels.shape) != (self.H, self.W)
+                    or not labels.is_contiguous()):
+                raise DmmError("labels must be a contiguous uint8 (H, W) tensor on the context device")
+            self._call("dmm_energy_of", frame, ctypes.c_void_p(labels.data_ptr()), ctypes.byref(e),
+                       _stream_handle(stream, self.device))
         return int(e.value)
 
     def run_host_frames(self, left, right, iterations: int = 4, labels_out=None, frame: int = 0, stream=None):
@@ -338,7 +348,7 @@ class Context:
         b = (ctypes.c_int64 * n)()
         self._call("dmm_run_host_frames", frame, n, ctypes.c_void_p(left.data_ptr()),
                    ctypes.c_void_p(right.data_ptr()), iterations, ctypes.c_void_p(labels_out.data_ptr()), e, b,
-                   _stream_handle(stream))
+                   _stream_handle(stream, self.device))
         for f in range(frame, frame + n):
             self._iters[f] = iterations
         return labels_out, [int(v) for v in e], [int(v) for v in b]
@@ -365,6 +375,6 @@ class Context:
         e = ctypes.c_int64()
         b = ctypes.c_int64()
         self._call("dmm_run_host", frame, ctypes.c_void_p(lp), ctypes.c_void_p(rp), iterations,
-                   ctypes.c_void_p(op), ctypes.byref(e), ctypes.byref(b), _stream_handle(stream))
+                   ctypes.c_void_p(op), ctypes.byref(e), ctypes.byref(b), _stream_handle(stream, self.device))
         self._iters[frame] = iterations
         return labels_out, int(e.value), int(b.value)

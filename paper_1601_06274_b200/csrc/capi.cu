@@ -33,12 +33,16 @@ struct dmm_ctx {
 
 namespace {
 
+constexpr int kPartial = -1;   // iters_done of a DMM_TUNE_DEBUG_STOP_AFTER_H solve
+
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 bool valid(const dmm_config* c) {
     if (!c) return false;
     const int K = c->d_max - c->d_min + 1;
-    return c->width >= 1 && c->height >= 1 && c->width <= (1 << 16) && c->height <= (1 << 16) &&
+    // width <= 16384: cost_kernel stages the row's two code rows (8 * W bytes) in
+    // shared memory; W * H <= 2^28 keeps every pixel index in int32.
+    return c->width >= 1 && c->height >= 1 && c->width <= (1 << 14) && c->height <= (1 << 14) &&
            K >= 1 && K <= 256 && (c->census_radius == 1 || c->census_radius == 2) &&
            c->w_h >= 0 && c->w_v >= 0 && c->w_h <= 255 && c->w_v <= 255 && c->trunc >= 1 &&
            c->frac_bits >= 0 && c->frac_bits <= 8 && c->oob_cost >= -1 && c->oob_cost <= 255 &&
@@ -104,6 +108,7 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->labels = (uint8_t*)take(px);
     off->bounds = (long long*)take(8 * 2 * (size_t)c->max_iters);
     off->energy = (long long*)take(8);
+    off->flag = (int32_t*)take(8);
     return o;
 }
 
@@ -140,6 +145,21 @@ struct Timed {
         }
     }
 };
+
+// Every entry point that takes a context runs on the context's device and
+// restores the caller's current device on return (contexts on
+// several devices in one thread).
+struct DevGuard {
+    int prev = -1;
+    bool sw = false;
+    explicit DevGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) sw = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DevGuard() {
+        if (sw) cudaSetDevice(prev);
+    }
+};
+#define DMM_DEVICE_GUARD(ctx) DevGuard dmm_dev_guard_((ctx)->device)
 
 dmm_status frame_ok(dmm_ctx* ctx, int frame, int n = 1) {
     if (!ctx || frame < 0 || n < 1 || frame + n > ctx->cfg.batch) {
@@ -212,6 +232,7 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.labels = (uint8_t*)(b + (size_t)off.labels);
     c->L.base.bounds = (long long*)(b + (size_t)off.bounds);
     c->L.base.energy = (long long*)(b + (size_t)off.energy);
+    c->L.base.flag = (int32_t*)(b + (size_t)off.flag);
     c->L.W = cfg->width; c->L.H = cfg->height; c->L.K = c->K; c->L.KP = c->KP;
     c->ws = b;
     c->ws_bytes = bytes;
@@ -222,7 +243,8 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->stop_after_h = 0;
     c->pair_ok = pair_range_ok(cfg);
     c->use_pair = 1;
-    if (cudaSetDevice(device) != cudaSuccess) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         dmm_destroy(c);
         return DMM_E_CUDA;
     }
@@ -241,6 +263,8 @@ void dmm_destroy(dmm_ctx* ctx) {
 
 dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right,
                            int64_t pitch, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
@@ -255,6 +279,8 @@ dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const u
 }
 
 dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
     if (st) return st;
     if (iterations < 1 || iterations > ctx->cfg.max_iters) {
@@ -278,10 +304,15 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
         }
         if (ctx->stop_after_h) break;
     }
+    if (ctx->stop_after_h) {   // debug: only f_ after H_1 is meaningful (dmm_copy_dual which = 0)
+        if ((st = check_launch(ctx, "solve"))) return st;
+        for (int f = frame; f < frame + nframes; ++f) ctx->iters_done[f] = kPartial;
+        return DMM_OK;
+    }
     {
         Timed tm(ctx, 4, s);
         dmm::launch_energy(ctx->L, frame, nframes, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc,
-                           ctx->cfg.frac_bits, s);
+                           ctx->cfg.frac_bits, nullptr, nullptr, s);
     }
     if ((st = check_launch(ctx, "solve"))) return st;
     for (int f = frame; f < frame + nframes; ++f) ctx->iters_done[f] = iterations;
@@ -290,9 +321,12 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
 
 dmm_status dmm_result(dmm_ctx* ctx, int frame, int64_t* energy, int64_t* bound,
                       int64_t* bound_history, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     const int it = ctx->iters_done[frame];
+    if (it == kPartial) { ctx->err = "partial (debug stop-after-H) solve has no result"; return DMM_E_STATE; }
     if (it < 1) { ctx->err = "result before solve"; return DMM_E_STATE; }
     cudaStream_t s = (cudaStream_t)stream;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
@@ -312,6 +346,8 @@ dmm_status dmm_result(dmm_ctx* ctx, int frame, int64_t* energy, int64_t* bound,
 }
 
 dmm_status dmm_copy_labels(dmm_ctx* ctx, int frame, uint8_t* labels, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!labels) return DMM_E_ARG;
@@ -324,6 +360,8 @@ dmm_status dmm_copy_labels(dmm_ctx* ctx, int frame, uint8_t* labels, void* strea
 }
 
 dmm_status dmm_copy_codes(dmm_ctx* ctx, int frame, int which, uint32_t* dst, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
@@ -336,6 +374,8 @@ dmm_status dmm_copy_codes(dmm_ctx* ctx, int frame, int which, uint32_t* dst, voi
 }
 
 dmm_status dmm_copy_cost_volume(dmm_ctx* ctx, int frame, uint8_t* dst, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!dst) return DMM_E_ARG;
@@ -346,10 +386,12 @@ dmm_status dmm_copy_cost_volume(dmm_ctx* ctx, int frame, uint8_t* dst, void* str
 }
 
 dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
-    if (ctx->iters_done[frame] < 1) return DMM_E_STATE;
+    if (ctx->iters_done[frame] == 0 || (ctx->iters_done[frame] == kPartial && which != 0)) return DMM_E_STATE;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
     dmm::launch_decode_rec(which ? P.fh : P.fv, which ? P.D : nullptr, ctx->cfg.frac_bits, dst,
                            (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
@@ -359,6 +401,8 @@ dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void*
 dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const uint8_t* right_host,
                         int32_t iterations, uint8_t* labels_host, int64_t* energy, int64_t* bound,
                         void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!left_host || !right_host || !labels_host) return DMM_E_ARG;
@@ -378,6 +422,8 @@ dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const
 
 dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left,
                                   const uint8_t* right, int64_t pitch, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
     if (st) return st;
     if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
@@ -393,6 +439,8 @@ dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const ui
 dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8_t* left_host,
                                const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
                                int64_t* energy, int64_t* bound, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
     if (st) return st;
     if (!left_host || !right_host || !labels_host || !energy || !bound) return DMM_E_ARG;
@@ -447,6 +495,8 @@ dmm_status dmm_buffer_ptr(dmm_ctx* ctx, int frame, int which, void** ptr, size_t
 }
 
 dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* D_dense, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!D_dense) return DMM_E_ARG;
@@ -460,6 +510,8 @@ dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* D_dens
 
 dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int vertical, int32_t iterations,
                          void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
     if (st) return st;
     if (iterations < 1 || iterations > ctx->cfg.max_iters || t < 0 || t >= iterations ||
@@ -485,21 +537,33 @@ dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int ve
 }
 
 dmm_status dmm_energy(dmm_ctx* ctx, int frame, int64_t* energy, void* stream) {
+    return dmm_energy_of(ctx, frame, nullptr, energy, stream);
+}
+
+dmm_status dmm_energy_of(dmm_ctx* ctx, int frame, const uint8_t* labels, int64_t* energy, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st) return st;
     if (!energy) return DMM_E_ARG;
     if (!ctx->has_cost[frame]) { ctx->err = "energy before cost volume"; return DMM_E_STATE; }
     cudaStream_t s = (cudaStream_t)stream;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    int* bad = P.flag;     // set by the kernel if a label is >= K
     long long e = 0;
+    int badh = 0;
     if ((st = cuda_err(ctx, cudaMemsetAsync(P.energy, 0, 8, s), "memset energy"))) return st;
+    if ((st = cuda_err(ctx, cudaMemsetAsync(bad, 0, 4, s), "memset flag"))) return st;
     {
         Timed tm(ctx, 4, s);
-        dmm::launch_energy(ctx->L, frame, 1, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc, ctx->cfg.frac_bits, s);
+        dmm::launch_energy(ctx->L, frame, 1, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc, ctx->cfg.frac_bits, labels,
+                           bad, s);
     }
     if ((st = check_launch(ctx, "energy"))) return st;
     if ((st = cuda_err(ctx, cudaMemcpyAsync(&e, P.energy, 8, cudaMemcpyDeviceToHost, s), "d2h"))) return st;
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(&badh, bad, 4, cudaMemcpyDeviceToHost, s), "d2h"))) return st;
     if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
+    if (badh) { ctx->err = "label index >= K"; return DMM_E_ARG; }
     *energy = e;
     return DMM_OK;
 }
@@ -508,7 +572,6 @@ int64_t dmm_launch_count(const dmm_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 dmm_status dmm_set_tuning(dmm_ctx* ctx, int param, int64_t value) {
     if (!ctx) return DMM_E_ARG;
-    if (param == DMM_TUNE_WAVE_BYTES && value >= 0) return DMM_OK;   // ignored (dmm.h)
     if (param == DMM_TUNE_DEBUG_STOP_AFTER_H) { ctx->stop_after_h = value != 0; return DMM_OK; }
     if (param == DMM_TUNE_PAIR) { ctx->use_pair = value != 0; return DMM_OK; }
     if (param == DMM_TUNE_QUERY_PAIR) { ctx->err = ctx->use_pair && ctx->pair_ok ? "pair" : "int32"; return DMM_OK; }

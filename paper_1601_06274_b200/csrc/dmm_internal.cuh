@@ -43,6 +43,7 @@ struct FramePtrs {
     uint8_t* labels;
     long long* bounds;   // [2 * max_iters]
     long long* energy;   // [1]
+    int32_t* flag;       // [1] scratch: label-range flag of dmm_energy_of
 };
 
 // Per-frame pointers are base + frame * stride (bytes).
@@ -70,6 +71,7 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.labels += o;
     p.bounds = (long long*)((char*)p.bounds + o);
     p.energy = (long long*)((char*)p.energy + o);
+    p.flag = (int32_t*)((char*)p.flag + o);
     return p;
 }
 
@@ -98,8 +100,10 @@ int hm_launches_per_pass(const PassArgs& a, int vertical, int wave);
 // valid when the configuration passes the pair range check (capi.cu).
 void launch_hm2_pass(const PassArgs& a, int vertical, int nframes, cudaStream_t s);
 int hm2_launches_per_pass(const PassArgs& a, int vertical);
+// labels == nullptr: the frames' own labels; else a caller labelling u8 [H][W]
+// (one frame); bad (nullable) is set to 1 if a label is >= K.
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
-                   cudaStream_t s);
+                   const uint8_t* labels, int32_t* bad, cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
 // dense u8 [cells][K] -> padded [cells][KP] (pads = 0)
 void launch_pad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);

@@ -6,17 +6,22 @@
 namespace dmm {
 
 __global__ void __launch_bounds__(256)
-energy_kernel(Layout L, int frame0, int w_h, int w_v, int T, int fbits) {
+energy_kernel(Layout L, int frame0, int w_h, int w_v, int T, int fbits, const uint8_t* __restrict__ ext,
+              int32_t* bad) {
     FramePtrs P = frame_ptrs(L, frame0 + blockIdx.y);
-    const int W = L.W, H = L.H, KP = L.KP;
+    const int W = L.W, H = L.H, KP = L.KP, K = L.K;
+    const uint8_t* __restrict__ lab = ext ? ext : P.labels;
     long long e = 0;
+    bool oob = false;
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < W * H; q += gridDim.x * blockDim.x) {
         const int y = q / W, x = q - y * W;
-        const int l = P.labels[q];
-        e += P.D[(size_t)q * KP + l];
-        if (x + 1 < W) e += (long long)w_h * min(abs(l - (int)P.labels[q + 1]), T);
-        if (y + 1 < H) e += (long long)w_v * min(abs(l - (int)P.labels[q + W]), T);
+        const int l = lab[q];
+        oob |= l >= K;
+        e += P.D[(size_t)q * KP + min(l, K - 1)];
+        if (x + 1 < W) e += (long long)w_h * min(abs(l - (int)lab[q + 1]), T);
+        if (y + 1 < H) e += (long long)w_v * min(abs(l - (int)lab[q + W]), T);
     }
+    if (oob && bad) *bad = 1;
     for (int d = 16; d > 0; d >>= 1) e += __shfl_down_sync(kFull, e, d);
     __shared__ long long part[8];
     if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = e;
@@ -29,10 +34,10 @@ energy_kernel(Layout L, int frame0, int w_h, int w_v, int T, int fbits) {
 }
 
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
-                   cudaStream_t s) {
+                   const uint8_t* labels, int32_t* bad, cudaStream_t s) {
     int blocks = (L.W * L.H + 255) / 256;
     if (blocks > 4 * 148) blocks = 4 * 148;
-    energy_kernel<<<dim3(blocks, nframes), 256, 0, s>>>(L, frame0, w_h, w_v, T, fbits);
+    energy_kernel<<<dim3(blocks, nframes), 256, 0, s>>>(L, frame0, w_h, w_v, T, fbits, labels, bad);
 }
 
 template <typename T>

@@ -371,3 +371,39 @@ def test_primitive_buffers_and_half_steps(orc):
     assert torch.equal(a.labels(), b.labels())
     assert a.result()[2] == [int(v) for v in b.bound_slots()[: 2 * iters].tolist()]
     assert a.result()[0] == b.energy()
+
+
+def test_energy_of_arbitrary_labelling(orc):
+    """dmm_energy_of (SPEC S:62-70 energy_evaluate; Eq.3) on random and
+    constant labellings equals the oracle's energy; labels >= K are rejected."""
+    import paper_1601_06274_b200 as dmm
+    W, H, K = 97, 41, 40
+    left, right, _ = datagen.pair("rd", W, H, K, seed=5)
+    ctx = _ctx(width=W, height=H, d_min=-3, d_max=K - 4, w_h=2, w_v=5, T=3, frac_bits=3)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    D = ctx.cost_volume_tensor().cpu().numpy()
+    rng = np.random.default_rng(0)
+    for lab in (rng.integers(0, K, size=(H, W)), np.zeros((H, W), np.int64), np.full((H, W), K - 1)):
+        lt = torch.from_numpy(lab.astype(np.uint8)).cuda()
+        assert ctx.energy(labels=lt) == orc.energy(D, lab.astype(np.int32), 2, 5, 3) << 3
+    bad = torch.full((H, W), K, dtype=torch.uint8, device="cuda")
+    with pytest.raises(dmm.DmmError):
+        ctx.energy(labels=bad)
+
+
+def test_partial_solve_has_no_result():
+    """DMM_TUNE_DEBUG_STOP_AFTER_H: f_ after H_1 is readable, the result is not."""
+    import paper_1601_06274_b200 as dmm
+    W, H, K = 40, 20, 16
+    left, right, _ = datagen.pair("rd", W, H, K, seed=2)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=2)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.set_stop_after_h(True)
+    ctx.solve(2)
+    ctx.dual(0)
+    for call in (lambda: ctx.result(), lambda: ctx.labels(), lambda: ctx.dual(1)):
+        with pytest.raises(dmm.DmmError):
+            call()
+    ctx.set_stop_after_h(False)
+    ctx.solve(2)
+    assert ctx.result()[1] <= ctx.result()[0]
