@@ -274,6 +274,38 @@ __device__ __forceinline__ void st_rec_pair(uint8_t* ra, uint8_t* rb, bool wb, i
     }
 }
 
+// As st_rec_pair, into shared-memory records at ra / rb (both always
+// written; the caller bulk-stores B only if the pair has a B chain).
+template <int LPL, bool PAD>
+__device__ __forceinline__ void st_rec_pair_s(unsigned ra, unsigned rb, int lane, const unsigned (&o)[LPL], int oa,
+                                              int ob, int K) {
+    constexpr int KP = 32 * LPL;
+    unsigned v[LPL];
+#pragma unroll
+    for (int e = 0; e < LPL; ++e) v[e] = (!PAD || lane * LPL + e < K) ? o[e] : 0u;
+    const unsigned pa = ra + 2 * LPL * lane;
+    const unsigned pb = rb + 2 * LPL * lane;
+    if constexpr (LPL == 1) {
+        sts16(pa, v[0] & 0xffffu);
+        sts16(pb, v[0] >> 16);
+    } else if constexpr (LPL == 2) {
+        sts32(pa, __byte_perm(v[0], v[1], 0x5410));
+        sts32(pb, __byte_perm(v[0], v[1], 0x7632));
+    } else if constexpr (LPL == 4) {
+        sts64(pa, make_uint2(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410)));
+        sts64(pb, make_uint2(__byte_perm(v[0], v[1], 0x7632), __byte_perm(v[2], v[3], 0x7632)));
+    } else {
+        sts128(pa, make_uint4(__byte_perm(v[0], v[1], 0x5410), __byte_perm(v[2], v[3], 0x5410),
+                              __byte_perm(v[4], v[5], 0x5410), __byte_perm(v[6], v[7], 0x5410)));
+        sts128(pb, make_uint4(__byte_perm(v[0], v[1], 0x7632), __byte_perm(v[2], v[3], 0x7632),
+                              __byte_perm(v[4], v[5], 0x7632), __byte_perm(v[6], v[7], 0x7632)));
+    }
+    if (lane == 0) {
+        sts32(ra + 2 * KP, (unsigned)oa);
+        sts32(rb + 2 * KP, (unsigned)ob);
+    }
+}
+
 // floor(z / 2) per signed 16-bit half
 __device__ __forceinline__ unsigned sra1_2(unsigned z) {
     const unsigned s = (unsigned)(((int)z) >> 1);
@@ -283,9 +315,17 @@ __device__ __forceinline__ unsigned sra1_2(unsigned z) {
 // Handshake (Alg.5, readings R9/R10) on a pair.  In: pl = message
 // into i from the left, pr = message into j from the right, (vi, bi*) and
 // (vj, bj*) = the node costs.  Out: pl = phi_ij, pr = phi_ji'.
-template <int LPL, bool PAD, int WIN>
+//
+// OPT: also return the two chains' optima min_k m_i(k) (optA, optB): with
+// pl / pr the exact messages from the chain ends (the root Handshake), m_i is
+// the min-marginal at i, whose minimum is the chain optimum F* -- which
+// equals the sum of the node minima of the hierarchical minorant (exactness,
+// Lemma 1; pinned by tests/test_oracle_chain.py), i.e. the chain's
+// share of the dual bound (Eq.7).
+template <int LPL, bool PAD, int WIN, bool OPT = false>
 __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, int bib, const unsigned (&vj)[LPL],
-                                           int bja, int bjb, MP<LPL>& pl, MP<LPL>& pr, const DtK<LPL>& k) {
+                                           int bja, int bjb, MP<LPL>& pl, MP<LPL>& pr, const DtK<LPL>& k,
+                                           int* opt = nullptr) {
     // phi_ji := Msg(f_j + phi_{j+1,j})
     unsigned pji[LPL];
 #pragma unroll
@@ -295,6 +335,14 @@ __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, i
         int g0, g1;
         dtrans2<LPL, PAD, WIN, false>(pji, k, g0, g1);
     }
+    if constexpr (OPT) {
+        unsigned l = kBigP;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e)
+            if (!PAD || k.lane * LPL + e < k.K) l = __vmins2(l, pl.m[e] + vi[e] + pji[e]);   // halves >= 0: no carry
+        opt[0] = __reduce_min_sync(kFull, lo16(l)) + pl.a + bia + ja;
+        opt[1] = __reduce_min_sync(kFull, hi16(l)) + pl.b + bib + jb;
+    }
     // t = floor((m_i - 2 phi_ji) / 2), m_i = phi_L + f_i + phi_ji; true offset C = pl.o + bi - pji.o
     const int ca = pl.a + bia - ja, cb = pl.b + bib - jb;
     const unsigned c0 = pk(ca & 1, cb & 1);
@@ -303,15 +351,15 @@ __device__ __forceinline__ void handshake2(const unsigned (&vi)[LPL], int bia, i
     for (int e = 0; e < LPL; ++e) t[e] = sra1_2(__vsub2(pl.m[e] + vi[e] + c0, pji[e]));
     int ta = ca >> 1, tb = cb >> 1;
     msg2<LPL, PAD, WIN>(t, ta, tb, k);                           // phi_ij
-    // phi_ji' = Msg(-phi_ij) = -maxplus(phi_ij); normalised: gmax - maxplus(t_n)
-    unsigned u[LPL];
+    // phi_ji' = Msg(-phi_ij) = -phi_ij: a Msg output is V-Lipschitz
+    // (phi(a) - phi(b) <= V(a,b), V = ws*min(|a-b|,T) is a metric), so
+    // max_a phi(a) - V(a,b) = phi(b) and Msg(-phi) = -phi exactly (DESIGN.md
+    // "Bounce identity"; pinned in tests/test_oracle_chain.py).  The
+    // normalised t lies in [0, wsT]; -t is stored as wsT - t >= 0 with the
+    // offset -t_off - wsT.
 #pragma unroll
-    for (int e = 0; e < LPL; ++e) u[e] = t[e];
-    int gA, gB;
-    const unsigned Gm = dtrans2<LPL, PAD, WIN, true>(u, k, gA, gB);
-#pragma unroll
-    for (int e = 0; e < LPL; ++e) { pr.m[e] = __vsub2(Gm, u[e]); pl.m[e] = t[e]; }
-    pr.a = -ta - gA; pr.b = -tb - gB;
+    for (int e = 0; e < LPL; ++e) { pr.m[e] = __vsub2(k.capP, t[e]); pl.m[e] = t[e]; }
+    pr.a = -ta - k.wsT; pr.b = -tb - k.wsT;
     pl.a = ta; pl.b = tb;
 }
 

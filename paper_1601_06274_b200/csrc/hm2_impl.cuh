@@ -288,12 +288,13 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         }
     }
     // Handshake; the ring delivers F_j then F_i.  Writes fwd[i+1] = phi_ij, bwd[i] = phi_ji'.
-    __device__ __forceinline__ void handshake(int i, MP<LPL>& pl, MP<LPL>& pr) {
+    template <bool OPT = false>
+    __device__ __forceinline__ void handshake(int i, MP<LPL>& pl, MP<LPL>& pr, int* opt = nullptr) {
         unsigned vi[LPL], vj[LPL];
         int bia, bib, bja, bjb;
         pop(vj, bja, bjb);
         pop(vi, bia, bib);
-        handshake2<LPL, PAD, WIN>(vi, bia, bib, vj, bja, bjb, pl, pr, this->dk);
+        handshake2<LPL, PAD, WIN, OPT>(vi, bia, bib, vj, bja, bjb, pl, pr, this->dk, opt);
         this->st_spine(true, i + 1, pl);
         this->st_spine(false, i, pr);
     }
@@ -331,7 +332,12 @@ __global__ void __launch_bounds__(64) hm2_root_kernel(PassArgs a) {
     if (warp == 0) {
         MP<LPL> pr;
         h.ld_spine(false, j, pr);
-        h.handshake(i, phi, pr);
+        int opt[2];
+        h.template handshake<true>(i, phi, pr, opt);
+        // the pair's share of the dual bound: the two chain optima (see handshake2)
+        if (lane == 0)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&h.P.bounds[a.bound_slot]),
+                      (unsigned long long)((long long)opt[0] + (h.hasB ? (long long)opt[1] : 0ll)));
     }
 }
 
@@ -379,12 +385,15 @@ __global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int 
 
 // ============================================================== leaf kernel
 struct LeafShared {     // per-warp shared memory (bytes)
-    int F, D, stack, mbar, total;
+    int F, D, O, stack, mbar, total;
     __host__ __device__ LeafShared(int KP, bool first) {
         const int srec = first ? KP : rec_bytes(KP);
         F = 0;                                     // kCMax source record pairs
         D = F + 2 * kCMax * srec;                  // kCMax D-row pairs (unused when FIRST)
-        stack = D + (first ? 0 : 2 * kCMax * KP);  // kDepth x (phi_ij, R) message pairs
+        // output record pairs: in place over F (a node's F is dead once it is
+        // emitted), except when FIRST (F = D rows, shorter than a record)
+        O = first ? D : F;
+        stack = first ? O + 2 * kCMax * rec_bytes(KP) : D + 2 * kCMax * KP;   // kDepth x (phi_ij, R) message pairs
         mbar = align_up(stack + kDepth * 2 * (4 * KP + 16), 8);
         total = align_up(mbar + 8, 128);
     }
@@ -405,48 +414,59 @@ __device__ __forceinline__ void ld_mp_s(const uint8_t* p, int lane, MP<LPL>& v) 
     v.a = o.x; v.b = o.y;
 }
 
-// Emit leaf `node` of both chains: lambda = L + F + R (R8); record L + R + D*2^F;
-// bound += min lambda; last V: lowest argmin as the label (R13, R14).
+// Emit leaf `node` of both chains: lambda = L + F + R (R8); the record
+// L + R + D*2^F goes to the shared-memory output slots oa / ob (bulk-stored
+// per block).  nodebound: bound += min lambda (only when no root Handshake
+// supplied the chain optima, lstar == 0); last V: lowest argmin as the label
+// (R13, R14).
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
 __device__ __forceinline__ void leaf_emit(const Pass<LPL, VERT, PAD, WIN, FIRST>& h, unsigned dA, unsigned dB,
-                                          int node, const MP<LPL>& Lb, const MP<LPL>& Rb, const unsigned (&F)[LPL],
-                                          int bfa, int bfb, bool last, long long& bsum) {
-    constexpr int REC = Pass<LPL, VERT, PAD, WIN, FIRST>::REC;
+                                          unsigned oA, unsigned oB, int node, const MP<LPL>& Lb, const MP<LPL>& Rb,
+                                          const unsigned (&F)[LPL], int bfa, int bfb, bool last, bool nodebound,
+                                          long long& bsum) {
     const int lane = h.lane;
-    unsigned Dv[LPL], o[LPL], lam[LPL];
+    unsigned Dv[LPL], o[LPL];
     if constexpr (FIRST) {      // the unaries are D*2^F themselves
 #pragma unroll
         for (int e = 0; e < LPL; ++e) Dv[e] = F[e];
     } else {
         ld_u8_pair_s<LPL>(dA, dB, lane, h.fbits, Dv);
     }
-    unsigned l = kBigP;
+    unsigned lr[LPL];
 #pragma unroll
     for (int e = 0; e < LPL; ++e) {
-        const unsigned lr = Lb.m[e] + Rb.m[e];
-        o[e] = lr + Dv[e];
-        lam[e] = lr + F[e];
-        if (!PAD || lane * LPL + e < h.K) l = __vmins2(l, lam[e]);
+        lr[e] = Lb.m[e] + Rb.m[e];
+        o[e] = lr[e] + Dv[e];
     }
     const int oa = Lb.a + Rb.a, ob = Lb.b + Rb.b;
-    st_rec_pair<LPL, PAD>(h.dst + (size_t)h.qA(node) * REC, h.dst + (size_t)h.qB(node) * REC, h.hasB, lane, o, oa,
-                          ob, h.K);
-    const int gA = __reduce_min_sync(kFull, lo16(l)), gB = __reduce_min_sync(kFull, hi16(l));
-    bsum += (long long)gA + oa + bfa;
-    if (h.hasB) bsum += (long long)gB + ob + bfb;
-    if (VERT && last) {
-        int ka = INT_MAX, kb = INT_MAX;
+    st_rec_pair_s<LPL, PAD>(oA, oB, lane, o, oa, ob, h.K);
+    if (nodebound || (VERT && last)) {
+        unsigned lam[LPL];
+        unsigned l = kBigP;
 #pragma unroll
-        for (int e = LPL - 1; e >= 0; --e) {
-            const bool ok = !PAD || lane * LPL + e < h.K;
-            if (ok && lo16(lam[e]) == gA) ka = lane * LPL + e;
-            if (ok && hi16(lam[e]) == gB) kb = lane * LPL + e;
+        for (int e = 0; e < LPL; ++e) {
+            lam[e] = lr[e] + F[e];
+            if (!PAD || lane * LPL + e < h.K) l = __vmins2(l, lam[e]);
         }
-        ka = __reduce_min_sync(kFull, ka);
-        kb = __reduce_min_sync(kFull, kb);
-        if (lane == 0) {
-            h.P.labels[h.qA(node)] = (uint8_t)ka;
-            if (h.hasB) h.P.labels[h.qB(node)] = (uint8_t)kb;
+        const int gA = __reduce_min_sync(kFull, lo16(l)), gB = __reduce_min_sync(kFull, hi16(l));
+        if (nodebound) {
+            bsum += (long long)gA + oa + bfa;
+            if (h.hasB) bsum += (long long)gB + ob + bfb;
+        }
+        if (VERT && last) {
+            int ka = INT_MAX, kb = INT_MAX;
+#pragma unroll
+            for (int e = LPL - 1; e >= 0; --e) {
+                const bool ok = !PAD || lane * LPL + e < h.K;
+                if (ok && lo16(lam[e]) == gA) ka = lane * LPL + e;
+                if (ok && hi16(lam[e]) == gB) kb = lane * LPL + e;
+            }
+            ka = __reduce_min_sync(kFull, ka);
+            kb = __reduce_min_sync(kFull, kb);
+            if (lane == 0) {
+                h.P.labels[h.qA(node)] = (uint8_t)ka;
+                if (h.hasB) h.P.labels[h.qB(node)] = (uint8_t)kb;
+            }
         }
     }
 }
@@ -464,11 +484,14 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
     constexpr int kStrideD = FIRST ? kStrideF : (VERT ? 2 * KP : KP);
     constexpr int kOffD = FIRST ? kOffF : (VERT ? KP : kCMax * KP);
     constexpr int SMP = 4 * KP + 16;
+    constexpr int REC = PS::REC;
+    constexpr int kStrideO = VERT ? 2 * REC : REC, kOffO = VERT ? REC : kCMax * REC;
     const LeafShared lay(KP, FIRST);
     char* wsm = smem + warp * lay.total;
     const unsigned wsa = smem_addr(wsm);
     const unsigned sF = wsa + lay.F;
     const unsigned sD = FIRST ? sF : wsa + lay.D;
+    const unsigned sO = wsa + lay.O;
     uint8_t* stk = reinterpret_cast<uint8_t*>(wsm + lay.stack);
     const unsigned bar = wsa + lay.mbar;
     if (lane == 0) { mbar_init(reinterpret_cast<uint64_t*>(wsm + lay.mbar), 1); fence_mbar_init(); }
@@ -480,6 +503,7 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
     PS h;
     h.init(a, lane);
     const int n = h.n;
+    const bool nodebound = lstar == 0;   // else the root Handshake added the chain optima
     bool waited = false;
     if (lstar == 0) {       // no root before this kernel: its records come from the previous kernel
         pdl_wait();
@@ -494,6 +518,8 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         task_bounds(n, lstar, b & (nbl - 1), lo0, hi0);
         const int m = hi0 - lo0 + 1;
         const unsigned bytes = 2 * m * SREC + (FIRST ? 0 : 2 * m * KP);
+        bulk_wait_read();    // the previous block's output bulk stores have read the staging slots
+        __syncwarp();
         if (lane == 0) mbar_expect_tx_s(bar, bytes);
         __syncwarp();
         fence_proxy_async();
@@ -542,7 +568,9 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         auto fA = [&](int k) { return sF + k * kStrideF; };
         auto dA = [&](int k) { return sD + k * kStrideD; };
         auto emit = [&](int k, const MP<LPL>& Lb, const MP<LPL>& Rb, const unsigned (&F)[LPL], int ba, int bb) {
-            leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(k), dA(k) + kOffD, lo0 + k, Lb, Rb, F, ba, bb, last, bsum);
+            const unsigned oa = sO + k * kStrideO;
+            leaf_emit<LPL, VERT, PAD, WIN, FIRST>(h, dA(k), dA(k) + kOffD, oa, oa + kOffO, lo0 + k, Lb, Rb, F, ba, bb,
+                                                  last, nodebound, bsum);
         };
         // pieces of <= 3 nodes: straight-line code (R5 with the splits unrolled)
         auto small = [&](int lo, int hi, const MP<LPL>& L, const MP<LPL>& R) {
@@ -646,8 +674,20 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
             hi = i;
             R = pr;
         }
+        // the block's output records: bulk stores from the staging slots
         __syncwarp();
+        fence_proxy_async();
+        __syncwarp();
+        if constexpr (!VERT) {
+            if (lane == 0) tma_store_s(h.dst + (size_t)h.qA(lo0) * REC, sO, m * REC);
+            if (lane == 1 && h.hasB) tma_store_s(h.dst + (size_t)h.qB(lo0) * REC, sO + kOffO, m * REC);
+        } else {
+            if (lane < m) tma_store_s(h.dst + (size_t)h.qA(lo0 + lane) * REC, sO + lane * kStrideO,
+                                      (h.hasB ? 2 : 1) * REC);
+        }
+        bulk_commit();
     }
+    bulk_wait_all();
     if (!waited) pdl_wait();
     if (lane == 0 && bsum != 0)
         atomicAdd(reinterpret_cast<unsigned long long*>(&h.P.bounds[a.bound_slot]), (unsigned long long)bsum);

@@ -244,6 +244,30 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+// ---- TMA bulk stores shared -> global (cp.async.bulk ... bulk_group)
+__device__ __forceinline__ void tma_store_s(void* dst, unsigned src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// this thread's committed bulk stores have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// ... and completed (writes performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void sts32(unsigned a, unsigned v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts16(unsigned a, unsigned v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts64(unsigned a, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts128(unsigned a, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------- Msg
 // Generic exact distance transform on a warp-held K-vector:
 //   MAX = false: x(b) := min_a x(a) + ws*min(|a-b|, T)      (Msg, min-plus)
@@ -341,11 +365,10 @@ __device__ __forceinline__ void handshake_regs(const int (&Fi)[LPL], const int (
 #pragma unroll
     for (int e = 0; e < LPL; ++e) t_[e] = (pl[e] + Fi[e] - pji[e]) >> 1;   // floor(m_i/2 - phi_ji)
     msg<LPL, PAD, WIN>(t_, ws, wsT, lane, K);                // phi_ij
+    // bounce back: Msg(-phi_ij) = -phi_ij exactly, because a Msg output is
+    // V-Lipschitz for the metric V = ws*min(|a-b|,T)
 #pragma unroll
-    for (int e = 0; e < LPL; ++e) pl[e] = t_[e];
-    dtrans<LPL, PAD, WIN, true>(t_, ws, wsT, lane, K);       // bounce back: Msg(-phi_ij) = -maxplus(phi_ij)
-#pragma unroll
-    for (int e = 0; e < LPL; ++e) pr[e] = -t_[e];
+    for (int e = 0; e < LPL; ++e) { pl[e] = t_[e]; pr[e] = -t_[e]; }
 }
 
 }  // namespace dmm

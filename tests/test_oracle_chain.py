@@ -53,6 +53,35 @@ def test_msg_symmetric_direction(orc):
         assert np.array_equal(orc.msg(a[::-1], 3, 4)[::-1], orc.msg(a, 3, 4))
 
 
+def test_msg_bounce_identity(orc):
+    """Msg(-Msg(t)) == -Msg(t): a Msg output phi is V-Lipschitz for the metric
+    V(a,b) = ws*min(|a-b|,T) (triangle inequality of min(|.|,T)), so
+    max_a phi(a) - V(a,b) = phi(b).  This is the identity the GPU Handshake
+    uses for Alg.5's bounce-back phi_ji' = Msg(-phi_ij) (P:820; DESIGN.md
+    "Bounce identity"); pinned here by O(K^2) enumeration, independently of the
+    oracle's DT, and it fails for a non-metric pairwise term (checked below)."""
+    rng = np.random.default_rng(11)
+
+    def msg_enum(a, V):
+        return np.array([min(a[x] + V[x][b] for x in range(len(a))) for b in range(len(a))])
+
+    for _ in range(1500):
+        K = int(rng.integers(1, 24))
+        ws = int(rng.integers(0, 60))
+        T = int(rng.integers(1, K + 3))
+        V = [[ws * min(abs(x - b), T) for b in range(K)] for x in range(K)]
+        t = rng.integers(-800, 800, size=K)
+        phi = msg_enum(t, V)
+        assert np.array_equal(msg_enum(-phi, V), -phi)
+        assert np.array_equal(orc.msg(-orc.msg(t, ws, T), ws, T), -orc.msg(t, ws, T))
+    # a non-metric pairwise term (squared distance) breaks it: the identity is
+    # a property of the truncated-linear (metric) regulariser, not of Msg
+    Vq = [[(x - b) ** 2 for b in range(3)] for x in range(3)]
+    t = np.array([0, 100, 100])
+    phi = msg_enum(t, Vq)
+    assert not np.array_equal(msg_enum(-phi, Vq), -phi)
+
+
 # ---------------------------------------------------------- min-marginals
 def test_min_marginals_paper_potts5(orc):
     """Paper-printed min-marginals, Potts strength 5."""
