@@ -386,42 +386,106 @@ def main():
 
 
 def run_bands(args, c, world, rank, local, dev):
-    """One frame sharded in row bands (H) / column bands (V) over all ranks,
-    all-to-all transposes over NCCL between half-steps."""
+    """One frame sharded in row bands (H) / column bands (V) over all ranks
+    (SURVEY 8(e)): dmm_shard(ROWCOL) -- the library's own NCCL communicator
+    does the all-to-all transposes between half-steps, the bound / energy
+    all-reduce and the labelling all-gather.  Strong scaling."""
     import torch
     import torch.distributed as dist
 
+    import paper_1601_06274_b200 as dmm
     from paper_1601_06274_b200 import sharding
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
     left, right, _ = datagen.pair(c["kind"], W, H, K, seed=0)       # the same frame on every rank
-    if world == 1 and not dist.is_initialized():
+    if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29561")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-    eng = sharding.CudaBandEngine(W, H, world, rank, d_min=0, d_max=K - 1, w=W_REG, T=T_REG,
-                                  frac_bits=FBITS, max_iters=iters, device=dev)
-    exch = sharding.DistExchanger()
+    ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
+                      max_iters=iters, device=dev, shard_world=world)
+    sharding.rowcol_setup(ctx)
+    stream = torch.cuda.current_stream(dev)
     lt = torch.from_numpy(left).to(dev)
     rt = torch.from_numpy(right).to(dev)
+
+    def step():
+        ctx.cost_volume(lt, rt, stream=stream)
+        ctx.solve(iters, stream=stream)
+
     for _ in range(args.warmup):
-        sharding.solve_bands(eng, exch, lt, rt, iters)
+        step()
+    torch.cuda.synchronize(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    launches = ctx.launch_count - launches0
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    energy, bound, hist = ctx.result()
+
+    # profiled pass: this rank's half-step kernels (its row band for H, its
+    # column band for V) -> roofline on the compact algorithmic bytes of its bands
+    prof_steps = max(1, min(args.steps, 20))
+    ctx.read_profile()
+    ctx.set_profiling(True)
+    for i in range(prof_steps):
+        flush.fill_(i & 0xff)
+        step()
+    torch.cuda.synchronize(dev)
+    ctx.set_profiling(False)
+    prof = ctx.read_profile()
+    r0, r1 = sharding.bands(H, world)[rank]
+    c0, c1 = sharding.bands(W, world)[rank]
+    hr, wc = r1 - r0, c1 - c0
+    cells_h, cells_v, px_h, px_v = hr * W * K, H * wc * K, hr * W, H * wc
+    alg = (3 * cells_h + 4 * px_h) + (iters - 1) * (5 * cells_h + 8 * px_h) + iters * (4 * cells_v + 8 * px_v) + px_v
+    hm_ms = (prof["hm_h"][0] + prof["hm_v"][0]) / prof_steps
+    hbm, peak_kind = peaks()
+    achieved = alg / (hm_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": "chain-DP half-step (root+level+leaf kernels), H and V, rank 0's bands",
+                "basis": "SURVEY 8(d) compact bytes of this rank's row band (H) and column band (V)",
+                "peak_kind": peak_kind, "hm_ms_per_step": hm_ms, "profiled_steps": prof_steps,
+                "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    # expected NVLink bytes per half-step: every rank sends (world-1)/world of its band's records
+    rec = 2 * (32 * (1 << max(0, (K - 1).bit_length() - 5))) + 16
+    xfer = (hr * W - hr * wc) * rec
+
+    # end to end with host buffers through the sharded context
+    lh = torch.from_numpy(left).pin_memory()
+    rh = torch.from_numpy(right).pin_memory()
+    lab = torch.empty((H, W), dtype=torch.uint8).pin_memory()
+    for _ in range(2):
+        ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
     torch.cuda.synchronize(dev)
     dist.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    sampler.start()
-    t0.record()
+    t0.record(stream)
+    w0 = time.perf_counter()
     for _ in range(args.steps):
-        labels, hist, energy = sharding.solve_bands(eng, exch, lt, rt, iters)
-    t1.record()
+        ctx.run_host(lh, rh, iters, labels_out=lab, stream=stream)
+    t1.record(stream)
     torch.cuda.synchronize(dev)
-    dist.barrier()
-    clocks = sampler.stop()
-    ms = t0.elapsed_time(t1) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    ems = max(t0.elapsed_time(t1) / args.steps, (time.perf_counter() - w0) * 1e3 / args.steps)
+    t = torch.tensor([ems], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ems = float(t.item())
     if rank == 0:
         cells = W * H * K
         line = {
@@ -429,10 +493,16 @@ def run_bands(args, c, world, rank, local, dev):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": f"{args.config}: one {W}x{H}x{K} frame sharded in {world} row/column bands, "
-                                   f"{iters} dual iterations, all-to-all transposes between half-steps",
-                       "W": W, "H": H, "K": K, "iters": iters, "fps": 1e3 / ms, "parallelism": f"bands x{world}"},
-            "roofline": None, "cpu_baseline": None, "e2e": None, "clocks": clocks,
-            "result": {"energy": energy / (1 << FBITS), "bound": hist[-1] / (1 << FBITS)},
+                                   f"{iters} dual iterations, NCCL all-to-all transposes between half-steps "
+                                   f"(dmm_shard ROWCOL)",
+                       "W": W, "H": H, "K": K, "iters": iters, "fps": 1e3 / ms, "parallelism": f"bands x{world}",
+                       "nvlink_bytes_per_half_step_per_rank": xfer,
+                       "l2": "flushed between timed steps (256 MB write outside events)"},
+            "roofline": roofline, "cpu_baseline": None,
+            "e2e": {"value": cells * iters / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * W * H,
+                    "d2h_bytes_per_step": W * H + 8 + 8, "ms_per_step": ems},
+            "clocks": clocks, "gpu_launches": launches,
+            "result": {"energy": energy / (1 << FBITS), "bound": bound / (1 << FBITS)},
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -194,6 +194,68 @@ DMM_API dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t
 DMM_API dmm_status dmm_energy(dmm_ctx* ctx, int frame, int64_t* energy, void* stream);
 DMM_API dmm_status dmm_energy_of(dmm_ctx* ctx, int frame, const uint8_t* labels, int64_t* energy, void* stream);
 
+/* ---- multi-GPU sharding (one process per GPU)
+ *
+ * dmm_nccl_unique_id: a fresh NCCL communicator id (128 bytes) on the
+ * calling rank (rank 0), to be broadcast to the other ranks by the caller
+ * (e.g. torch.distributed).  NCCL is loaded at run time (libnccl.so.2: the
+ * process's own, e.g. torch's, else the system's); DMM_E_NCCL if unavailable.
+ *
+ * dmm_shard(ctx, id, rank, world, mode) makes ctx rank `rank` of `world`:
+ *  - DMM_SHARD_FRAMES: the caller gives every rank its own frames (contexts
+ *    are independent, no data-path collective); only records rank/world and,
+ *    if id != NULL, creates the communicator.
+ *  - DMM_SHARD_ROWCOL: ONE frame (batch == 1) solved by all ranks.  Rank r
+ *    owns rows [r*H/world .. ) for the H half-steps and columns [r*W/world ..)
+ *    for the V half-steps (band sizes differ by <= 1; every column band
+ *    >= 16 wide).  Chains of one orientation are independent, so the
+ *    only exchange is the transpose of the dual records between half-steps:
+ *    one grouped ncclSend / ncclRecv all-to-all per half-step, issued by the
+ *    library on the call's stream; the bound history and energy are int64
+ *    sums combined by ncclAllReduce and the labelling is all-gathered, so
+ *    dmm_result / dmm_copy_labels / dmm_run_host return the whole frame's
+ *    results on every rank, bit-identical to the unsharded solve.  Each rank
+ *    computes the cost volume of its own row band and column band only.
+ *    The context must have been created with the frame's full config and a
+ *    workspace of >= dmm_shard_workspace_bytes(cfg, rank, world, mode)
+ *    bytes (<= dmm_workspace_bytes for world >= 2); the packed chain-pair
+ *    kernels must apply (DMM_TUNE_PAIR on, 16-bit range check) -- else DMM_E_ARG.
+ *    dmm_shard with id == NULL creates no communicator ("external
+ *    transport"): dmm_solve then returns DMM_E_STATE and the caller drives
+ *    dmm_half_step and moves the bytes of dmm_shard_plan itself (tests).
+ *    Full-frame parity taps (dmm_copy_cost_volume, dmm_copy_dual,
+ *    dmm_buffer_ptr, dmm_import_cost_volume, dmm_energy_of, the *_frames
+ *    calls) return DMM_E_STATE on a ROWCOL context.
+ *  ncclCommInitRank is collective: every rank must call dmm_shard.
+ *
+ * Host-only (no device, no context; usable on CPU hosts):
+ * dmm_shard_workspace_bytes: workspace a ROWCOL rank needs (0 if invalid).
+ * dmm_shard_plan: the all-to-all of half-step `phase` (0: after H, f_
+ *   records row band -> column band; 1: after V, D*2^F + g_ records back) as
+ *   one dmm_xfer per peer (self included): byte ranges relative to the
+ *   workspace base; returns the number of entries (= world; -1 on bad
+ *   arguments), writes at most `max`.  Every range is contiguous.
+ * dmm_shard_locate: byte offset (from the workspace base) of pixel (y, x)'s
+ *   record / label in rank `rank`'s arrays (DMM_LOC_*), -1 if not owned. */
+#define DMM_SHARD_FRAMES 0
+#define DMM_SHARD_ROWCOL 1
+#define DMM_LOC_FV_H 0     /* H band output records (f_), column segments */
+#define DMM_LOC_FH_H 1     /* H band input records (D*2^F + g_)          */
+#define DMM_LOC_FV_V 2     /* V band input records (f_)                  */
+#define DMM_LOC_FH_V 3     /* V band output records (D*2^F + g_)         */
+#define DMM_LOC_LABEL_V 4  /* V band labels (u8)                         */
+#define DMM_LOC_BOUNDS 5   /* int64 bound history [2*max_iters] + energy  */
+typedef struct dmm_xfer {
+    int32_t peer;
+    int64_t send_offset, send_bytes;   /* to peer   */
+    int64_t recv_offset, recv_bytes;   /* from peer */
+} dmm_xfer;
+DMM_API dmm_status dmm_nccl_unique_id(uint8_t out[128]);
+DMM_API dmm_status dmm_shard(dmm_ctx* ctx, const uint8_t* id, int rank, int world, int mode);
+DMM_API size_t dmm_shard_workspace_bytes(const dmm_config* cfg, int rank, int world, int mode);
+DMM_API int dmm_shard_plan(const dmm_config* cfg, int rank, int world, int phase, dmm_xfer* out, int max);
+DMM_API int64_t dmm_shard_locate(const dmm_config* cfg, int rank, int world, int which, int y, int x);
+
 /* Number of kernels this context has launched since creation. */
 DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
 

@@ -28,7 +28,10 @@ EXPORTS = (
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
     "dmm_cost_volume_frames", "dmm_run_host_frames", "dmm_energy_of",
+    "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
 )
+SHARD_FRAMES, SHARD_ROWCOL = 0, 1
+LOC_FV_H, LOC_FH_H, LOC_FV_V, LOC_FH_V, LOC_LABEL_V, LOC_BOUNDS = range(6)
 BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
 TUNE_STOP_AFTER_H = 2
 TUNE_PAIR = 3
@@ -44,6 +47,17 @@ class DmmConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "width", "height", "d_min", "d_max", "census_radius", "w_h", "w_v", "trunc",
         "frac_bits", "oob_cost", "batch", "max_iters")]
+
+
+class DmmXfer(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("send_offset", ctypes.c_int64), ("send_bytes", ctypes.c_int64),
+                ("recv_offset", ctypes.c_int64), ("recv_bytes", ctypes.c_int64)]
+
+
+def make_config(width, height, d_min=0, d_max=127, w=3, T=4, frac_bits=4, census_radius=2, oob_cost=-1,
+                batch=1, max_iters=16, w_h=None, w_v=None) -> DmmConfig:
+    return DmmConfig(width, height, d_min, d_max, census_radius, w if w_h is None else w_h,
+                     w if w_v is None else w_v, T, frac_bits, oob_cost, batch, max_iters)
 
 
 def library_path() -> str:
@@ -89,6 +103,11 @@ def load_library():
         "dmm_half_step": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, i32, ctypes.c_int, i32, P]),
         "dmm_energy": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(i64), P]),
         "dmm_energy_of": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.POINTER(i64), P]),
+        "dmm_nccl_unique_id": (ctypes.c_int, [P]),
+        "dmm_shard": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "dmm_shard_workspace_bytes": (ctypes.c_size_t, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "dmm_shard_plan": (ctypes.c_int, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int]),
+        "dmm_shard_locate": (i64, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -96,6 +115,31 @@ def load_library():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL communicator id (dmm_nccl_unique_id), to broadcast to the other ranks."""
+    buf = (ctypes.c_uint8 * 128)()
+    _prim_check(load_library().dmm_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def shard_workspace_bytes(cfg: DmmConfig, rank: int, world: int, mode: int = SHARD_ROWCOL) -> int:
+    return int(load_library().dmm_shard_workspace_bytes(ctypes.byref(cfg), rank, world, mode))
+
+
+def shard_plan(cfg: DmmConfig, rank: int, world: int, phase: int):
+    """dmm_shard_plan (host only): [(peer, send_off, send_bytes, recv_off, recv_bytes)] of one all-to-all."""
+    out = (DmmXfer * world)()
+    n = load_library().dmm_shard_plan(ctypes.byref(cfg), rank, world, phase, out, world)
+    if n < 0:
+        raise DmmError("dmm_shard_plan: invalid arguments")
+    return [(x.peer, x.send_offset, x.send_bytes, x.recv_offset, x.recv_bytes) for x in out[:n]]
+
+
+def shard_locate(cfg: DmmConfig, rank: int, world: int, which: int, y: int, x: int) -> int:
+    """dmm_shard_locate (host only): byte offset of pixel (y, x)'s record / label, -1 if not owned."""
+    return int(load_library().dmm_shard_locate(ctypes.byref(cfg), rank, world, which, y, x))
 
 
 def torch_int64():
@@ -147,7 +191,7 @@ class Context:
     def __init__(self, width: int, height: int, d_min: int = 0, d_max: int = 127, w: int = 3,
                  T: int = 4, frac_bits: int = 4, census_radius: int = 2, oob_cost: int = -1,
                  batch: int = 1, max_iters: int = 16, w_h: int | None = None,
-                 w_v: int | None = None, device=None):
+                 w_v: int | None = None, device=None, shard_world: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise DmmError("no CUDA device: the DMM hot path has no CPU fallback")
@@ -161,9 +205,15 @@ class Context:
         nbytes = self._lib.dmm_workspace_bytes(ctypes.byref(self.cfg))
         if nbytes == 0:
             raise DmmError("invalid dmm_config")
+        if shard_world >= 1:
+            # room for a later ROWCOL shard() over shard_world ranks, any rank
+            nbytes = max([nbytes] + [int(self._lib.dmm_shard_workspace_bytes(ctypes.byref(self.cfg), r,
+                                                                             shard_world, SHARD_ROWCOL))
+                                     for r in range(shard_world)])
         self.workspace = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
+        self._base_off = aligned - base
         h = ctypes.c_void_p()
         self._check(self._lib.dmm_create(ctypes.byref(self.cfg), ctypes.c_void_p(aligned), nbytes,
                                          self.device.index, ctypes.byref(h)), None)
@@ -285,6 +335,21 @@ class Context:
         out = torch.empty((self.H, self.W, self.K), dtype=torch.int32, device=self.device)
         self._call("dmm_copy_dual", frame, which, ctypes.c_void_p(out.data_ptr()), _stream_handle(stream, self.device))
         return out
+
+    # --------------------------------------------------------- multi-GPU
+    def shard(self, nccl_id: bytes | None, rank: int, world: int, mode: int = SHARD_ROWCOL):
+        """dmm_shard: make this context rank `rank` of `world` (ROWCOL: one frame
+        in row / column bands, the all-to-all transposes and reductions done
+        by the library over NCCL).  nccl_id None: no communicator (the caller
+        moves the bytes of shard_plan between dmm_half_step calls)."""
+        idbuf = None if nccl_id is None else (ctypes.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._call("dmm_shard", idbuf, rank, world, mode)
+        self.rank, self.world, self.shard_mode = rank, world, mode
+
+    def ws_view(self, offset: int, nbytes: int):
+        """uint8 view of `nbytes` bytes at byte `offset` of the (aligned) workspace."""
+        o = self._base_off + offset
+        return self.workspace[o: o + nbytes]
 
     # ------------------------------------------------ sharding building blocks
     def buffer(self, which: int, frame: int = 0):

@@ -10,26 +10,7 @@
 #include "../../include/dmm.h"
 #include "dmm_internal.cuh"
 
-struct dmm_ctx {
-    dmm_config cfg;
-    int K, KP, device, oob;
-    dmm::Layout L;
-    char* ws;
-    size_t ws_bytes;
-    // per-frame host state
-    int* has_cost;
-    int* iters_done;
-    long long launches;
-    std::string err;
-    // event profiling (dmm_set_profiling)
-    int profiling;
-    int stop_after_h;     // debug: dmm_solve runs only the first H half-step
-    int pair_ok;          // configuration passes pair_range_ok
-    int use_pair;         // DMM_TUNE_PAIR (default 1): packed chain-pair kernels when pair_ok
-    struct Rec { int cls; cudaEvent_t a, b; };
-    std::vector<Rec> recs;
-    std::vector<cudaEvent_t> pool;
-};
+#include "ctx.cuh"
 
 namespace {
 
@@ -169,11 +150,19 @@ dmm_status frame_ok(dmm_ctx* ctx, int frame, int n = 1) {
     return DMM_OK;
 }
 
-// One half-step (vertical = 0: H, 1: V) of iteration t on frames [frame, frame+nframes).
-void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations, cudaStream_t s) {
+}  // namespace
+
+namespace dmm {
+
+dmm_status cuda_status(dmm_ctx* ctx, cudaError_t e, const char* where) { return cuda_err(ctx, e, where); }
+
+// One half-step (vertical = 0: H, 1: V) of iteration t on frames [frame,
+// frame+nframes) of layout L (the context's frames, or a shard's band).
+dmm_status launch_half_on(dmm_ctx* ctx, const Layout& L, int frame, int nframes, int t, int v, int iterations,
+                          int nseg, const int* segx, cudaStream_t s) {
     const int T = ctx->cfg.trunc < ctx->K ? ctx->cfg.trunc : ctx->K;   // T >= K: untruncated
-    dmm::PassArgs a;
-    a.L = ctx->L;
+    PassArgs a;
+    a.L = L;
     a.frame0 = frame;
     a.fbits = ctx->cfg.frac_bits;
     a.ws = (v ? ctx->cfg.w_v : ctx->cfg.w_h) << ctx->cfg.frac_bits;
@@ -182,13 +171,32 @@ void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterati
     a.first = (t == 0 && v == 0);
     a.last = (t == iterations - 1 && v == 1);
     a.bound_slot = 2 * t + v;
+    a.nseg = nseg;
+    a.segx = segx;
     if (ctx->use_pair && ctx->pair_ok) {
-        Timed tm(ctx, 2 + v, s, dmm::hm2_launches_per_pass(a, v));
-        dmm::launch_hm2_pass(a, v, nframes, s);
-        return;
+        Timed tm(ctx, 2 + v, s, hm2_launches_per_pass(a, v));
+        launch_hm2_pass(a, v, nframes, s);
+    } else {
+        Timed tm(ctx, 2 + v, s, hm_launches_per_pass(a, v, 0));
+        launch_hm_pass(a, v, nframes, 0, s);
     }
-    Timed tm(ctx, 2 + v, s, dmm::hm_launches_per_pass(a, v, 0));
-    dmm::launch_hm_pass(a, v, nframes, 0, s);
+    return check_launch(ctx, "half step");
+}
+
+}  // namespace dmm
+
+namespace {
+
+void launch_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations, cudaStream_t s) {
+    dmm::launch_half_on(ctx, ctx->L, frame, nframes, t, v, iterations, 1, nullptr, s);
+}
+
+bool rowcol(const dmm_ctx* ctx) { return ctx->sh.mode == DMM_SHARD_ROWCOL; }
+
+dmm_status not_sharded(dmm_ctx* ctx, const char* what) {
+    if (!rowcol(ctx)) return DMM_OK;
+    ctx->err = std::string(what) + " is not available on a band-sharded context";
+    return DMM_E_STATE;
 }
 
 }  // namespace
@@ -256,6 +264,7 @@ void dmm_destroy(dmm_ctx* ctx) {
     if (!ctx) return;
     for (auto& r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);
+    dmm::shard_release(ctx);
     delete[] ctx->has_cost;
     delete[] ctx->iters_done;
     delete ctx;
@@ -270,8 +279,13 @@ dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const u
     if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
     if (pitch < ctx->cfg.width) { ctx->err = "pitch < width"; return DMM_E_SHAPE; }
     cudaStream_t s = (cudaStream_t)stream;
-    { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, 1, ctx->cfg.census_radius, pitch, left, right, s); }
-    { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, 1, ctx->cfg.d_min, ctx->oob, s); }
+    if (rowcol(ctx)) {
+        Timed t(ctx, 1, s, ctx->sh.world > 1 ? 3 : 2);
+        if ((st = dmm::shard_cost_volume(ctx, left, right, pitch, s))) return st;
+    } else {
+        { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, 1, ctx->cfg.census_radius, pitch, left, right, s); }
+        { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, 1, ctx->cfg.d_min, ctx->oob, s); }
+    }
     if ((st = check_launch(ctx, "cost_volume"))) return st;
     ctx->has_cost[frame] = 1;
     ctx->iters_done[frame] = 0;
@@ -290,6 +304,12 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
     for (int f = frame; f < frame + nframes; ++f)
         if (!ctx->has_cost[f]) { ctx->err = "solve before cost volume"; return DMM_E_STATE; }
     cudaStream_t s = (cudaStream_t)stream;
+    if (rowcol(ctx)) {
+        if (ctx->stop_after_h) { ctx->err = "stop-after-H is not available on a band-sharded context"; return DMM_E_STATE; }
+        if ((st = dmm::shard_solve(ctx, iterations, s))) return st;
+        ctx->iters_done[0] = iterations;
+        return DMM_OK;
+    }
     {   // bound history + energy of every frame: one strided memset
         dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
         const size_t row = (size_t)((char*)P.energy - (char*)P.bounds) + 8;
@@ -330,12 +350,14 @@ dmm_status dmm_result(dmm_ctx* ctx, int frame, int64_t* energy, int64_t* bound,
     if (it < 1) { ctx->err = "result before solve"; return DMM_E_STATE; }
     cudaStream_t s = (cudaStream_t)stream;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    long long* bptr = rowcol(ctx) ? ctx->sh.bounds : P.bounds;
+    long long* eptr = rowcol(ctx) ? ctx->sh.bounds + 2 * it : P.energy;
     long long e = 0;
     if (energy &&
-        (st = cuda_err(ctx, cudaMemcpyAsync(&e, P.energy, 8, cudaMemcpyDeviceToHost, s), "d2h")))
+        (st = cuda_err(ctx, cudaMemcpyAsync(&e, eptr, 8, cudaMemcpyDeviceToHost, s), "d2h")))
         return st;
     long long hist[2 * 1024];
-    if ((st = cuda_err(ctx, cudaMemcpyAsync(hist, P.bounds, 8 * 2 * (size_t)it, cudaMemcpyDeviceToHost, s),
+    if ((st = cuda_err(ctx, cudaMemcpyAsync(hist, bptr, 8 * 2 * (size_t)it, cudaMemcpyDeviceToHost, s),
                        "d2h bounds")))
         return st;
     if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
@@ -354,7 +376,8 @@ dmm_status dmm_copy_labels(dmm_ctx* ctx, int frame, uint8_t* labels, void* strea
     if (ctx->iters_done[frame] < 1) { ctx->err = "labels before solve"; return DMM_E_STATE; }
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
     return cuda_err(ctx,
-                    cudaMemcpyAsync(labels, P.labels, (size_t)ctx->L.W * ctx->L.H,
+                    cudaMemcpyAsync(labels, rowcol(ctx) ? ctx->sh.labels_full : P.labels,
+                                    (size_t)ctx->L.W * ctx->L.H,
                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
                     "copy labels");
 }
@@ -367,6 +390,7 @@ dmm_status dmm_copy_codes(dmm_ctx* ctx, int frame, int which, uint32_t* dst, voi
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
     if (!ctx->has_cost[frame]) return DMM_E_STATE;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    if (rowcol(ctx)) { P.codes_l = ctx->sh.codes_l; P.codes_r = ctx->sh.codes_r; }
     return cuda_err(ctx,
                     cudaMemcpyAsync(dst, which ? P.codes_r : P.codes_l, 4 * (size_t)ctx->L.W * ctx->L.H,
                                     cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
@@ -377,6 +401,7 @@ dmm_status dmm_copy_cost_volume(dmm_ctx* ctx, int frame, uint8_t* dst, void* str
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_copy_cost_volume"))) return st;
     if (st) return st;
     if (!dst) return DMM_E_ARG;
     if (!ctx->has_cost[frame]) return DMM_E_STATE;
@@ -389,6 +414,7 @@ dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void*
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_copy_dual"))) return st;
     if (st) return st;
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
     if (ctx->iters_done[frame] == 0 || (ctx->iters_done[frame] == kPartial && which != 0)) return DMM_E_STATE;
@@ -408,6 +434,7 @@ dmm_status dmm_run_host(dmm_ctx* ctx, int frame, const uint8_t* left_host, const
     if (!left_host || !right_host || !labels_host) return DMM_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    if (rowcol(ctx)) { P.img_l = ctx->sh.img_l; P.img_r = ctx->sh.img_r; P.labels = ctx->sh.labels_full; }
     const size_t px = (size_t)ctx->L.W * ctx->L.H;
     if ((st = cuda_err(ctx, cudaMemcpyAsync(P.img_l, left_host, px, cudaMemcpyHostToDevice, s), "h2d")))
         return st;
@@ -425,6 +452,7 @@ dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const ui
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st || (st = not_sharded(ctx, "dmm_cost_volume_frames"))) return st;
     if (st) return st;
     if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
     if (pitch < ctx->cfg.width) { ctx->err = "pitch < width"; return DMM_E_SHAPE; }
@@ -442,6 +470,7 @@ dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame, nframes);
+    if (st || (st = not_sharded(ctx, "dmm_run_host_frames"))) return st;
     if (st) return st;
     if (!left_host || !right_host || !labels_host || !energy || !bound) return DMM_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
@@ -474,6 +503,7 @@ dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8
 
 dmm_status dmm_buffer_ptr(dmm_ctx* ctx, int frame, int which, void** ptr, size_t* bytes, int* bytes_per_pixel) {
     dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_buffer_ptr"))) return st;
     if (st) return st;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
     const size_t px = (size_t)ctx->L.W * ctx->L.H;
@@ -498,6 +528,7 @@ dmm_status dmm_import_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* D_dens
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_import_cost_volume"))) return st;
     if (st) return st;
     if (!D_dense) return DMM_E_ARG;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
@@ -522,6 +553,14 @@ dmm_status dmm_half_step(dmm_ctx* ctx, int frame, int nframes, int32_t t, int ve
     for (int f = frame; f < frame + nframes; ++f)
         if (!ctx->has_cost[f]) { ctx->err = "half step before cost volume"; return DMM_E_STATE; }
     cudaStream_t s = (cudaStream_t)stream;
+    if (rowcol(ctx)) {     // this rank's band; the caller moves the records (dmm_shard_plan)
+        if (frame != 0 || nframes != 1) return DMM_E_ARG;
+        if ((st = cuda_err(ctx, cudaMemsetAsync(ctx->sh.bounds + 2 * t + vertical, 0, 8, s), "memset bound slot")))
+            return st;
+        if ((st = dmm::shard_half_step(ctx, t, vertical, iterations, s))) return st;
+        if (vertical && t == iterations - 1) ctx->iters_done[0] = iterations;
+        return DMM_OK;
+    }
     {   // reset this half-step's bound slot of every frame
         dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
         if ((st = cuda_err(ctx, cudaMemset2DAsync(P.bounds + 2 * t + vertical, ctx->L.frame_bytes, 0, 8,
@@ -544,6 +583,7 @@ dmm_status dmm_energy_of(dmm_ctx* ctx, int frame, const uint8_t* labels, int64_t
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_energy_of"))) return st;
     if (st) return st;
     if (!energy) return DMM_E_ARG;
     if (!ctx->has_cost[frame]) { ctx->err = "energy before cost volume"; return DMM_E_STATE; }
@@ -614,6 +654,7 @@ const char* dmm_status_str(dmm_status s) {
         case DMM_E_STATE: return "invalid state";
         case DMM_E_CUDA: return "CUDA error";
         case DMM_E_RANGE: return "numeric range";
+        case DMM_E_NCCL: return "NCCL error";
     }
     return "unknown";
 }

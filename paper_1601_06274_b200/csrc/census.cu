@@ -3,10 +3,8 @@
 //
 // census_kernel: one thread per pixel, 2-D 32x8 tiles staged through shared
 // memory with a replicated (clamped) border of `radius` pixels (reading R17).
-// cost_kernel: one CTA per image row; the row's left and right codes are
-// staged in shared memory and every thread emits 16 consecutive labels of one
-// pixel as a single 16-byte store, so a warp writes 512 contiguous bytes of the
-// label-contiguous volume D[y][x][KP] (coalesced, vectorised).
+// cost_kernel: one CTA per 64-pixel tile of a row (any rectangle of the
+// frame: the whole frame, or a rank's row / column band); see below.
 #include "dmm_internal.cuh"
 
 namespace dmm {
@@ -56,50 +54,94 @@ void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t
     census_kernel<<<grid, dim3(kTX, kTY), 0, s>>>(L, frame0, radius, pitch, left, right);
 }
 
-// D[y][x][k] = popc(cL[y][x] ^ cR[y][x - d_min - k]) or oob; pads (k >= K) = 0.
-__global__ void __launch_bounds__(256) cost_kernel(Layout L, int frame0, int d_min, int oob) {
-    extern __shared__ uint32_t srow[];   // [2][W]
-    const int f = frame0 + blockIdx.z, y = blockIdx.x;
-    FramePtrs P = frame_ptrs(L, f);
-    const int W = L.W, K = L.K, KP = L.KP;
-    uint32_t* sl = srow;
-    uint32_t* sr = srow + W;
-    for (int x = threadIdx.x; x < W; x += blockDim.x) {
-        sl[x] = P.codes_l[(size_t)y * W + x];
-        sr[x] = P.codes_r[(size_t)y * W + x];
+// D[y][x][k] = popc(cL[y][x] ^ cR[y][x - d_min - k]) or oob; pads (k >= K) = 0,
+// over the rectangle [x0, x0 + w) x [y0, y0 + h) of a frame whose codes are
+// full-frame rows of W codes; D rows of the rectangle have pitch w*KP.  One CTA
+// per (64-pixel tile, row, frame): the tile's left codes and the right codes
+// it can reach (64 + KP - 1) are staged in shared memory; thread (pixel, label
+// group) computes 16 labels of its pixel (consecutive lanes = consecutive
+// pixels: conflict-free code reads) into a padded shared tile (row stride
+// KP + 16 bytes: conflict-free 16-byte stores), which the CTA then copies out
+// row-major with 16-byte coalesced stores (a warp writes 512 contiguous
+// bytes).  Out-of-image samples are a select, not a branch.
+constexpr int kCostTX = 64;
+
+__global__ void __launch_bounds__(256)
+cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ codes_r, size_t code_fstride,
+            int W, int K, int KP, int d_min, int oob, int x0, int y0, int w, uint8_t* __restrict__ D,
+            size_t d_fstride) {
+    __shared__ uint32_t sl[kCostTX];
+    __shared__ uint32_t sr[kCostTX + 256];
+    __shared__ __align__(16) uint8_t tile[kCostTX * (256 + 16)];
+    const int tx0 = x0 + blockIdx.x * kCostTX;            // first pixel of the tile (frame x)
+    const int y = y0 + blockIdx.y;
+    const size_t fo = (size_t)blockIdx.z * code_fstride + (size_t)y * W;
+    const int npx = min(kCostTX, x0 + w - tx0);
+    const int base = tx0 - d_min - (KP - 1);               // frame x of sr[0]
+    for (int j = threadIdx.x; j < kCostTX + KP - 1; j += blockDim.x) {
+        const int xr = base + j;
+        sr[j] = (xr >= 0 && xr < W) ? codes_r[fo + xr] : 0u;
+        if (j < npx) sl[j] = codes_l[fo + tx0 + j];
     }
     __syncthreads();
-    const int chunks = KP / 16;
-    uint4* out = reinterpret_cast<uint4*>(P.D + (size_t)y * W * KP);
-    // blockIdx.y splits the row's output into gridDim.y contiguous parts
-    const int nq = W * chunks, per = (nq + gridDim.y - 1) / gridDim.y;
-    const int q0 = blockIdx.y * per, q1 = min(nq, q0 + per);
-    for (int q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
-        const int x = q / chunks, k0 = (q % chunks) * 16;
-        const uint32_t cl = sl[x];
-        uint32_t w[4];
+    const int chunks = KP / 16, stride = KP + 16;
+    const int px = threadIdx.x & (kCostTX - 1);
+    const int x = tx0 + px;
+    const uint32_t cl = sl[px];
+    // CTA-uniform fast path: every sample of the tile inside the image and no
+    // padded labels (all but the ~KP/64 border tiles of a row when K == KP):
+    // per label one shared load, XOR, POPC and a byte-packing IMAD
+    const bool fast = base >= 0 && tx0 + kCostTX - 1 - d_min < W && K == KP;
+    for (int c = threadIdx.x / kCostTX; c < chunks; c += blockDim.x / kCostTX) {
+        const int k0 = 16 * c;
+        uint32_t wv[4];
+        if (fast) {
+            const int s0 = px + KP - 1 - k0;          // sr index of label k0 (label k at s0 - (k - k0))
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            uint32_t v = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int k = k0 + g * 4 + b;
-                const int xr = x - d_min - k;
-                uint32_t c = (xr >= 0 && xr < W) ? (uint32_t)__popc(cl ^ sr[xr]) : (uint32_t)oob;
-                if (k >= K) c = 0;
-                v |= c << (8 * b);
+            for (int g = 0; g < 4; ++g) {
+                uint32_t v = __popc(cl ^ sr[s0 - 4 * g - 3]);
+                v = v * 256u + __popc(cl ^ sr[s0 - 4 * g - 2]);
+                v = v * 256u + __popc(cl ^ sr[s0 - 4 * g - 1]);
+                wv[g] = v * 256u + __popc(cl ^ sr[s0 - 4 * g]);
             }
-            w[g] = v;
+        } else {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int k = k0 + g * 4 + b;
+                    const int xr = x - d_min - k;
+                    const uint32_t cst =
+                        (unsigned)xr < (unsigned)W ? (uint32_t)__popc(cl ^ sr[xr - base]) : (uint32_t)oob;
+                    v |= (k < K ? cst : 0u) << (8 * b);
+                }
+                wv[g] = v;
+            }
         }
-        out[q] = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(tile + px * stride + k0) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+    __syncthreads();
+    uint4* out = reinterpret_cast<uint4*>(D + (size_t)blockIdx.z * d_fstride +
+                                          ((size_t)blockIdx.y * w + (tx0 - x0)) * KP);
+    for (int q = threadIdx.x; q < npx * chunks; q += blockDim.x) {
+        const int p = q / chunks, c = q - p * chunks;
+        out[q] = *reinterpret_cast<const uint4*>(tile + p * stride + 16 * c);
     }
 }
 
+void launch_cost_rect(const uint32_t* codes_l, const uint32_t* codes_r, size_t code_fstride, int W, int K, int KP,
+                      int d_min, int oob, int x0, int y0, int w, int h, uint8_t* D, size_t d_fstride, int nframes,
+                      cudaStream_t s) {
+    if (w <= 0 || h <= 0) return;
+    dim3 grid((w + kCostTX - 1) / kCostTX, h, nframes);
+    cost_kernel<<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, KP, d_min, oob, x0, y0, w, D, d_fstride);
+}
+
 void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s) {
-    const size_t smem = 2 * (size_t)L.W * sizeof(uint32_t);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cost_kernel<<<dim3(L.H, 4, nframes), 256, smem, s>>>(L, frame0, d_min, oob);
+    FramePtrs P = frame_ptrs(L, frame0);
+    launch_cost_rect(P.codes_l, P.codes_r, L.frame_bytes / 4, L.W, L.K, L.KP, d_min, oob, 0, 0, L.W, L.H, P.D,
+                     L.frame_bytes, nframes, s);
 }
 
 }  // namespace dmm

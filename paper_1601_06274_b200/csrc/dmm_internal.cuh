@@ -85,12 +85,23 @@ struct PassArgs {
     int first;        // H pass of iteration 0: g_ == 0, not read
     int last;         // V pass of the last iteration: write labels
     int bound_slot;   // index into bounds[]
+    // H records in column segments (band-sharded contexts, dmm_shard): the
+    // records of row c, position p live at segx[s]*H + c*(segx[s+1]-segx[s]) +
+    // (p - segx[s]) for the segment s containing p; nseg <= 1: row-major.
+    int nseg;
+    const int* segx;  // device [nseg + 1]
 };
 
 // kernels (launchers in the .cu files)
 void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t pitch,
                    const uint8_t* left, const uint8_t* right, cudaStream_t s);
 void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s);
+// Cost volume of the rectangle [x0, x0+w) x [y0, y0+h) of nframes frames:
+// codes are full-frame rows of W (frame stride code_fstride elements), D rows
+// of the rectangle have pitch w*KP (frame stride d_fstride bytes).
+void launch_cost_rect(const uint32_t* codes_l, const uint32_t* codes_r, size_t code_fstride, int W, int K, int KP,
+                      int d_min, int oob, int x0, int y0, int w, int h, uint8_t* D, size_t d_fstride, int nframes,
+                      cudaStream_t s);
 // One H (vertical = 0) or V (vertical = 1) half-step over all chains, launched
 // in waves of `wave` chains (0 = all at once); returns nothing, launches
 // hm_launches_per_pass() kernels.

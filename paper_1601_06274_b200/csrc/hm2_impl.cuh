@@ -70,6 +70,7 @@ struct Pass {
         n = VERT ? a.L.H : a.L.W;
         nch = VERT ? a.L.W : a.L.H;
         fbits = a.fbits; ws = a.ws; wsT = a.wsT;
+        nseg = a.nseg; segx = a.segx;
         dk.init(ws, wsT, K, lane);
     }
     __device__ __forceinline__ void set_pair(int pc) {
@@ -77,7 +78,27 @@ struct Pass {
         hasB = cA + 1 < nch;
         cB = hasB ? cA + 1 : cA;
     }
+    int nseg;
+    const int* segx;
     __device__ __forceinline__ int q_of(int c, int p) const { return VERT ? p * W + c : c * W + p; }
+    // record index of (chain c, position p) in the records the pass writes
+    // (and, unless FIRST, reads): row-major, or column segments for H records
+    // of a band-sharded context (PassArgs::segx)
+    __device__ __forceinline__ size_t rq(int c, int p) const {
+        if (VERT || nseg <= 1) return (size_t)q_of(c, p);
+        int s = 0;
+        while (p >= segx[s + 1]) ++s;
+        const int x0 = segx[s], w = segx[s + 1] - x0;
+        return (size_t)x0 * nch + (size_t)c * w + (p - x0);
+    }
+    __device__ __forceinline__ size_t srcq(int c, int p) const { return FIRST ? (size_t)q_of(c, p) : rq(c, p); }
+    // number of records contiguous with (c, p) in a run of cnt ascending positions
+    __device__ __forceinline__ int run1(int p, int cnt, bool segmented) const {
+        if (VERT || nseg <= 1 || !segmented) return cnt;
+        int s = 0;
+        while (p >= segx[s + 1]) ++s;
+        return min(cnt, segx[s + 1] - p);
+    }
     __device__ __forceinline__ int qA(int p) const { return q_of(cA, p); }
     __device__ __forceinline__ int qB(int p) const { return q_of(cB, p); }
     __device__ __forceinline__ void msg_(unsigned (&x)[LPL], int& oa, int& ob) const {
@@ -144,12 +165,17 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         __syncwarp();
         fence_proxy_async();
         __syncwarp();
-        if constexpr (!VERT) {   // H: the A and B runs are contiguous -> two bulk copies
+        if constexpr (!VERT) {   // H: the A and B runs are contiguous -> two bulk copies (four across a segment edge)
             const int first = r_dir > 0 ? r_start : r_start - cnt + 1;
-            if (this->lane == 0)
-                tma_load_s(sbase, this->src + (size_t)this->qA(first) * SREC, cnt * SREC, bar);
-            else if (this->lane == 1)
-                tma_load_s(sbase + kOffB, this->src + (size_t)this->qB(first) * SREC, cnt * SREC, bar);
+            const int n1 = this->run1(first, cnt, !FIRST);
+            const int ln = this->lane;
+            if (ln < 2 || (ln < 4 && n1 < cnt)) {
+                const int c = (ln & 1) ? this->cB : this->cA;
+                const int p = ln < 2 ? first : first + n1;
+                const int nn = ln < 2 ? n1 : cnt - n1;
+                tma_load_s(sbase + (ln & 1) * kOffB + (ln < 2 ? 0 : n1 * SREC),
+                           this->src + this->srcq(c, p) * SREC, nn * SREC, bar);
+            }
         } else {
             const int k = this->lane & 15;
             if (k < cnt) {
@@ -526,8 +552,13 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         __syncwarp();
         if constexpr (!VERT) {
             const size_t qa = (size_t)h.qA(lo0), qb = (size_t)h.qB(lo0);
-            if (lane == 0) tma_load_s(sF, h.src + qa * SREC, m * SREC, bar);
-            if (lane == 1) tma_load_s(sF + kOffF, h.src + qb * SREC, m * SREC, bar);
+            const int n1 = h.run1(lo0, m, !FIRST);
+            if (lane < 2 || (lane >= 4 && lane < 6 && n1 < m)) {
+                const int c = (lane & 1) ? h.cB : h.cA;
+                const int p = lane < 2 ? lo0 : lo0 + n1;
+                tma_load_s(sF + (lane & 1) * kOffF + (lane < 2 ? 0 : n1 * SREC), h.src + h.srcq(c, p) * SREC,
+                           (lane < 2 ? n1 : m - n1) * SREC, bar);
+            }
             if (!FIRST && lane == 2) tma_load_s(sD, h.P.D + qa * KP, m * KP, bar);
             if (!FIRST && lane == 3) tma_load_s(sD + kOffD, h.P.D + qb * KP, m * KP, bar);
         } else {
@@ -679,8 +710,13 @@ __global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lst
         fence_proxy_async();
         __syncwarp();
         if constexpr (!VERT) {
-            if (lane == 0) tma_store_s(h.dst + (size_t)h.qA(lo0) * REC, sO, m * REC);
-            if (lane == 1 && h.hasB) tma_store_s(h.dst + (size_t)h.qB(lo0) * REC, sO + kOffO, m * REC);
+            const int n1 = h.run1(lo0, m, true);
+            if ((lane < 2 || (lane < 4 && n1 < m)) && ((lane & 1) == 0 || h.hasB)) {
+                const int c = (lane & 1) ? h.cB : h.cA;
+                const int p = lane < 2 ? lo0 : lo0 + n1;
+                tma_store_s(h.dst + h.rq(c, p) * REC, sO + (lane & 1) * kOffO + (lane < 2 ? 0 : n1 * REC),
+                            (lane < 2 ? n1 : m - n1) * REC);
+            }
         } else {
             if (lane < m) tma_store_s(h.dst + (size_t)h.qA(lo0 + lane) * REC, sO + lane * kStrideO,
                                       (h.hasB ? 2 : 1) * REC);

@@ -332,22 +332,103 @@ def test_handshake_primitive(orc, K):
 
 
 # ------------------------------------------------------- band sharding (8e)
-@pytest.mark.parametrize("world", [1, 2, 3])
-def test_band_sharded_lockstep_equals_unsharded(orc, world):
-    """Row/column band decomposition on the CUDA path (all ranks' contexts in
-    one process, transposes as data movement): bit-identical to the
-    unsharded solve and to the oracle."""
+def _rowcol_lockstep(cfg_kw, left, right, iters, world):
+    """All ranks' ROWCOL contexts in one process (external transport): every
+    rank runs its band half-step through dmm_half_step, then the test moves
+    the bytes of dmm_shard_plan between the ranks' workspaces (pure data
+    movement, no kernel waits on another rank).  Returns the assembled
+    labelling and the summed bound history."""
+    import paper_1601_06274_b200 as dmm
+    H, W = left.shape
+    cfg = dmm.make_config(W, H, **cfg_kw)
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    ctxs = []
+    for r in range(world):
+        c = _ctx(width=W, height=H, shard_world=world, **cfg_kw)
+        c.shard(None, r, world, dmm.SHARD_ROWCOL)
+        c.cost_volume(lt, rt)
+        ctxs.append(c)
+
+    def exchange(phase):
+        plans = [dmm.shard_plan(cfg, r, world, phase) for r in range(world)]
+        for r in range(world):
+            for peer, so, sb, ro, rb in plans[r]:
+                # rank r sends [so, so+sb) to peer; peer receives it at its recv offset from r
+                pr = plans[peer][r]
+                assert pr[4] == sb
+                ctxs[peer].ws_view(pr[3], sb).copy_(ctxs[r].ws_view(so, sb))
+
+    for t in range(iters):
+        for c in ctxs:
+            c.half_step(t, 0, iters)
+        if world > 1:
+            exchange(0)
+        for c in ctxs:
+            c.half_step(t, 1, iters)
+        if world > 1 and t + 1 < iters:
+            exchange(1)
+    torch.cuda.synchronize()
+    labels = np.zeros((H, W), np.int32)
+    hist = np.zeros(2 * iters, np.int64)
+    for r, c in enumerate(ctxs):
+        boff = dmm.shard_locate(cfg, r, world, dmm.LOC_BOUNDS, 0, 0)
+        hist += c.ws_view(boff, 16 * iters).view(torch.int64).cpu().numpy()
+        c0, c1 = sharding_bands(W, world)[r]
+        off = dmm.shard_locate(cfg, r, world, dmm.LOC_LABEL_V, 0, c0)
+        labels[:, c0:c1] = c.ws_view(off, H * (c1 - c0)).view(H, c1 - c0).cpu().numpy()
+    return labels, hist
+
+
+def sharding_bands(n, world):
     from paper_1601_06274_b200 import sharding
+    return sharding.bands(n, world)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_rowcol_lockstep_equals_oracle(orc, world):
+    """ROWCOL band sharding through the C ABI (dmm_shard, dmm_half_step,
+    dmm_shard_plan; segmented H records written by the kernels' bulk stores):
+    labels and the whole bound history bit-identical to the oracle."""
     W, H, K, iters = 131, 47, 64, 3
     left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=11)
-    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
-    engines = [sharding.CudaBandEngine(W, H, world, r, d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4,
-                                       max_iters=iters) for r in range(world)]
-    labels, hist, energy = sharding.solve_bands_lockstep(engines, lt, rt, iters)
+    labels, hist = _rowcol_lockstep(dict(d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4, max_iters=iters),
+                                    left, right, iters, world)
     o = _run_oracle(orc, left, right, 0, K, 3, 3, 4, 4, iters)
-    assert np.array_equal(labels.cpu().numpy().astype(np.int32), o["labels"])
-    assert np.array_equal(np.array(hist), o["bound_hist"])
-    assert energy == o["energy"]
+    assert np.array_equal(labels, o["labels"])
+    assert np.array_equal(hist, o["bound_hist"])
+
+
+def test_rowcol_lockstep_c3_shape(orc):
+    """K = 256, bands crossing the leaf blocks at segment edges (world 3 of a
+    70-wide frame: segments of 24/23/23 columns), 2 iterations."""
+    W, H, K, iters = 70, 41, 256, 2
+    left, right, _ = datagen.pair("wt-middlebury", W, H, K, seed=4)
+    labels, hist = _rowcol_lockstep(dict(d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4, max_iters=iters),
+                                    left, right, iters, 3)
+    o = _run_oracle(orc, left, right, 0, K, 3, 3, 4, 4, iters)
+    assert np.array_equal(labels, o["labels"])
+    assert np.array_equal(hist, o["bound_hist"])
+
+
+def test_rowcol_nccl_world1(orc):
+    """The NCCL path on one GPU: dmm_nccl_unique_id + dmm_shard(ROWCOL, world 1)
+    + dmm_solve (all-reduce of bounds / energy, labels) == the oracle, and the
+    host-buffer end-to-end call on the sharded context."""
+    import paper_1601_06274_b200 as dmm
+    W, H, K, iters = 96, 40, 48, 3
+    left, right, _ = datagen.pair("rd", W, H, K, seed=9)
+    c = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=iters, shard_world=1)
+    c.shard(dmm.nccl_unique_id(), 0, 1, dmm.SHARD_ROWCOL)
+    c.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    c.solve(iters)
+    e, b, hist = c.result()
+    o = _run_oracle(orc, left, right, 0, K, 3, 3, 4, 4, iters)
+    assert np.array_equal(c.labels().cpu().numpy().astype(np.int32), o["labels"])
+    assert hist == [int(v) for v in o["bound_hist"]] and e == o["energy"]
+    lab, e2, b2 = c.run_host(left, right, iters)
+    assert np.array_equal(lab.numpy().astype(np.int32), o["labels"]) and (e2, b2) == (e, b)
+    with pytest.raises(dmm.DmmError):
+        c.dual(0)
 
 
 def test_primitive_buffers_and_half_steps(orc):

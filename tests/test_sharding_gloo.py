@@ -1,11 +1,16 @@
-"""Multi-rank (N > 1) paths on the CPU: band decomposition of Algorithm 2 with
-an all-to-all transpose between half-steps over torch.distributed (gloo,
-world size 2 and 3), and the frame assignment of frames mode.
+"""Multi-rank (N > 1) host logic on the CPU: the band partition, the frame
+assignment, and the C ABI's band-sharding plan (dmm_shard_plan /
+dmm_shard_locate, host-only entry points of libdmm_b200.so) driven through a
+real multi-process exchange over torch.distributed (gloo, world 2 and 3).
 
-The per-band half-steps here are an oracle engine (test infrastructure:
-oracle.hm per chain on dense int64 duals); the transposes, reductions and the
-driver are the product code of paper_1601_06274_b200.sharding.  The sharded
-result must be bit-identical to the unsharded oracle solve."""
+The exchange moves every record of a rank's H band to the rank owning its
+column in the V band (and back) -- a pure permutation of records.  Each
+process stamps its H band records with their pixel coordinates at the offsets
+dmm_shard_locate gives, executes dmm_shard_plan's transfers with
+dist.isend / dist.irecv (own block: a local copy), and checks that every V band
+slot received exactly the record of its pixel.  The GPU side (the kernels
+reading / writing those offsets, bit-exact vs the oracle) is
+tests/test_gpu_parity.py::test_rowcol_*."""
 import os
 import socket
 
@@ -15,6 +20,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import paper_1601_06274_b200 as dmm
 from paper_1601_06274_b200 import sharding
 
 
@@ -34,123 +40,137 @@ def test_frames_for_rank():
         assert got == list(range(n))
 
 
-class OracleBandEngine:
-    """One rank's share of a band-sharded solve, computed with the oracle."""
-
-    def __init__(self, D, w, T, Fb, world, rank):
-        import oracle
-        self.orc = oracle
-        H, W, K = D.shape
-        self.row_bands, self.col_bands = sharding.bands(H, world), sharding.bands(W, world)
-        self.rank = rank
-        (self.r0, self.r1), (self.c0, self.c1) = self.row_bands[rank], self.col_bands[rank]
-        self.Ds = torch.from_numpy(D.astype(np.int64) << Fb)
-        self.ws, self.T = w << Fb, T
-        self.fh_rb = self.Ds[self.r0:self.r1].clone()              # D*2^F + g_ (g_ = 0)
-        self.fv_rb = torch.zeros_like(self.fh_rb)
-        self.fv_cb = torch.zeros((H, self.c1 - self.c0, K), dtype=torch.int64)
-        self.fh_cb = torch.zeros_like(self.fv_cb)
-        self.labels = torch.zeros((H, self.c1 - self.c0), dtype=torch.int64)
-        self.partial = None
-
-    def half_h(self, t, iterations):
-        if self.partial is None:
-            self.partial = torch.zeros(2 * iterations, dtype=torch.int64)
-        for y in range(self.r1 - self.r0):
-            F = self.fh_rb[y].numpy()
-            h = self.orc.hm(F, self.ws, self.T)
-            # f_ = h - g_ = h - (F - D_s)
-            self.fv_rb[y] = torch.from_numpy(h - F) + self.Ds[self.r0 + y]
-            self.partial[2 * t] += int(h.min(1).sum())
-
-    def half_v(self, t, iterations):
-        for x in range(self.c1 - self.c0):
-            F = self.fv_cb[:, x].numpy()
-            v = self.orc.hm(F, self.ws, self.T)
-            g = torch.from_numpy(v - F)
-            self.fh_cb[:, x] = self.Ds[:, self.c0 + x] + g
-            self.partial[2 * t + 1] += int(v.min(1).sum())
-            if t == iterations - 1:
-                self.labels[:, x] = torch.from_numpy(v.argmin(1))
-
-    def fv_rows(self):
-        return self.fv_rb
-
-    def set_fv_cols(self, x):
-        self.fv_cb.copy_(x)
-
-    def fh_cols(self):
-        return self.fh_cb
-
-    def set_fh_rows(self, x):
-        self.fh_rb.copy_(x)
+def _cfg(W=67, H=13, K=40):
+    return dmm.make_config(W, H, 0, K - 1, max_iters=4)
 
 
-def _problem():
-    rng = np.random.default_rng(7)
-    return rng.integers(0, 25, size=(9, 13, 5)).astype(np.uint8), 3, 2, 4, 3
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+def test_locate_owns_each_pixel_once(world):
+    """Every pixel's H record is owned by the rank of its row band, its V
+    record by the rank of its column band (sharding.bands), at distinct,
+    record-aligned offsets inside the rank's workspace."""
+    cfg = _cfg()
+    W, H = cfg.width, cfg.height
+    rows, cols = sharding.bands(H, world), sharding.bands(W, world)
+    rec = 2 * 64 + 16
+    for r in range(world):
+        total = dmm.shard_workspace_bytes(cfg, r, world)
+        assert total > 0
+        for which, owned in ((dmm.LOC_FV_H, lambda y, x: rows[r][0] <= y < rows[r][1]),
+                             (dmm.LOC_FH_V, lambda y, x: cols[r][0] <= x < cols[r][1])):
+            offs = []
+            for y in range(H):
+                for x in range(W):
+                    o = dmm.shard_locate(cfg, r, world, which, y, x)
+                    assert (o >= 0) == owned(y, x)
+                    if o >= 0:
+                        assert 0 <= o and o + rec <= total
+                        offs.append(o)
+            offs = np.sort(np.array(offs))
+            assert np.all(np.diff(offs) >= rec)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5])
+def test_plan_pairs_up(world):
+    """Rank r's send to s has exactly the size of s's receive from r, and the
+    blocks one rank sends (phase 0) tile its H band's record array."""
+    cfg = _cfg(W=16 * world + 9, H=7 + world)
+    plans = [[dmm.shard_plan(cfg, r, world, ph) for ph in (0, 1)] for r in range(world)]
+    rec = 2 * 64 + 16
+    for ph in (0, 1):
+        for r in range(world):
+            assert [p[0] for p in plans[r][ph]] == list(range(world))
+            for s in range(world):
+                assert plans[r][ph][s][2] == plans[s][ph][r][4]
+        for r in range(world):
+            sends = sorted((p[1], p[2]) for p in plans[r][ph])
+            rows = sharding.bands(cfg.height, world)[r]
+            cols = sharding.bands(cfg.width, world)[r]
+            n_rec = (rows[1] - rows[0]) * cfg.width if ph == 0 else cfg.height * (cols[1] - cols[0])
+            assert sum(b for _, b in sends) == n_rec * rec
+            assert all(sends[k][0] + sends[k][1] == sends[k + 1][0] for k in range(world - 1))
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _stamp(ws, off, y, x, tag):
+    ws[off: off + 12] = np.frombuffer(np.array([y, x, tag], np.int32).tobytes(), np.uint8)
+
+
+def _read(ws, off):
+    return tuple(int(v) for v in np.frombuffer(ws[off: off + 12].tobytes(), np.int32))
+
+
+def _exchange(ws, plan, rank):
+    reqs, bufs = [], []
+    for peer, so, sb, ro, rb in plan:
+        if peer == rank:
+            ws[ro: ro + rb] = ws[so: so + sb].copy()
+            continue
+        if sb:
+            reqs.append(dist.isend(torch.from_numpy(ws[so: so + sb].copy()), peer))
+        if rb:
+            buf = torch.empty(rb, dtype=torch.uint8)
+            reqs.append(dist.irecv(buf, peer))
+            bufs.append((ro, buf))
+    for q in reqs:
+        q.wait()
+    for ro, buf in bufs:
+        ws[ro: ro + buf.numel()] = buf.numpy()
 
 
 def _worker(rank, world, port, q):
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        D, w, T, Fb, iters = _problem()
-        eng = OracleBandEngine(D, w, T, Fb, world, rank)
-        exch = sharding.DistExchanger()
-        sharding.band_dmm(eng, exch, iters)
-        hist = exch.all_reduce_sum(eng.partial.clone())
-        H = D.shape[0]
-        wmax = max(c1 - c0 for c0, c1 in eng.col_bands)
-        pad = torch.zeros((H, wmax), dtype=torch.int64)
-        pad[:, : eng.labels.shape[1]] = eng.labels
-        labs = exch.all_gather(pad)
-        labels = torch.cat([l[:, : c1 - c0] for l, (c0, c1) in zip(labs, eng.col_bands)], dim=1)
-        fpad = torch.zeros((H, wmax, D.shape[2]), dtype=torch.int64)
-        fpad[:, : eng.fv_cb.shape[1]] = eng.fv_cb
-        fv = torch.cat([f[:, : c1 - c0] for f, (c0, c1) in zip(exch.all_gather(fpad), eng.col_bands)], dim=1)
-        if rank == 0:
-            q.put((hist.numpy(), labels.numpy(), fv.numpy()))
-    finally:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        cfg = _cfg(W=16 * world + 21, H=9 + 2 * world, K=33)
+        W, H = cfg.width, cfg.height
+        ws = np.zeros(dmm.shard_workspace_bytes(cfg, rank, world), np.uint8)
+        bad = 0
+        # phase 0: H band f_ records -> V band
+        for y in range(H):
+            for x in range(W):
+                o = dmm.shard_locate(cfg, rank, world, dmm.LOC_FV_H, y, x)
+                if o >= 0:
+                    _stamp(ws, o, y, x, 100)
+        _exchange(ws, dmm.shard_plan(cfg, rank, world, 0), rank)
+        for y in range(H):
+            for x in range(W):
+                o = dmm.shard_locate(cfg, rank, world, dmm.LOC_FV_V, y, x)
+                if o >= 0 and _read(ws, o) != (y, x, 100):
+                    bad += 1
+        # phase 1: V band D*2^F + g_ records -> H band
+        for y in range(H):
+            for x in range(W):
+                o = dmm.shard_locate(cfg, rank, world, dmm.LOC_FH_V, y, x)
+                if o >= 0:
+                    _stamp(ws, o, y, x, 200)
+        _exchange(ws, dmm.shard_plan(cfg, rank, world, 1), rank)
+        for y in range(H):
+            for x in range(W):
+                o = dmm.shard_locate(cfg, rank, world, dmm.LOC_FH_H, y, x)
+                if o >= 0 and _read(ws, o) != (y, x, 200):
+                    bad += 1
+        dist.barrier()
         dist.destroy_process_group()
+        q.put((rank, bad))
+    except Exception as e:  # pragma: no cover - reported through the queue
+        q.put((rank, repr(e)))
 
 
 @pytest.mark.parametrize("world", [2, 3])
-def test_band_sharded_equals_unsharded_gloo(orc, world):
-    D, w, T, Fb, iters = _problem()
+def test_plan_exchange_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    hist, labels, fv = q.get(timeout=180)
+    res = dict(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
-        assert p.exitcode == 0
-    ref = orc.dmm(D, w, w, T, Fb, iters)
-    assert np.array_equal(hist, ref["bound_hist"])
-    assert np.array_equal(labels, ref["labels"])
-    assert np.array_equal(fv, ref["fdual"])
-
-
-def test_band_lockstep_equals_unsharded(orc):
-    """The same decomposition driven in one process (lockstep_band_dmm)."""
-    D, w, T, Fb, iters = _problem()
-    for world in (1, 2, 4):
-        engines = [OracleBandEngine(D, w, T, Fb, world, r) for r in range(world)]
-        sharding.lockstep_band_dmm(engines, iters)
-        hist = sum(e.partial for e in engines)
-        labels = torch.cat([e.labels for e in engines], dim=1)
-        ref = orc.dmm(D, w, w, T, Fb, iters)
-        assert np.array_equal(hist.numpy(), ref["bound_hist"])
-        assert np.array_equal(labels.numpy(), ref["labels"])
+    assert res == {r: 0 for r in range(world)}, res
