@@ -117,11 +117,46 @@ def warped_texture(W: int, H: int, max_disp: int, seed: int = 0, scene: str = "k
     return left, right, disp.astype(np.int32)
 
 
+def flow_pair(W: int, H: int, max_flow: int = 16, seed: int = 0):
+    """Optical-flow pair (configs[3]): I1 = a warped texture,
+    flow u = a smooth affine field plus two moving boxes, integer and within
+    [-max_flow, max_flow - 1] per component; I2 is built so that
+    I2(x + u1, y + u2) = I1(x, y): the texture sampled at the displaced
+    coordinates, with a z-order-free backward construction (I1 samples the
+    texture at x + u, I2 is the texture itself) plus independent N(0, 2^2)
+    noise.  Returns (I1, I2, u1, u2) as uint8, uint8, int32, int32 (H, W)."""
+    rng = np.random.default_rng(seed)
+    pad = max_flow + 2
+    tex = _texture(rng, H + 2 * pad, W + 2 * pad)
+    ys, xs = np.mgrid[0:H, 0:W]
+    a = rng.uniform(-0.5, 0.5, size=6)
+    u1 = a[0] * max_flow * 0.5 + a[1] * max_flow * (xs - W / 2) / W + a[2] * max_flow * (ys - H / 2) / H
+    u2 = a[3] * max_flow * 0.5 + a[4] * max_flow * (xs - W / 2) / W + a[5] * max_flow * (ys - H / 2) / H
+    for _ in range(2):
+        h = int(rng.integers(max(2, H // 8), max(3, H // 3)))
+        w = int(rng.integers(max(2, W // 10), max(3, W // 4)))
+        y0 = int(rng.integers(0, max(1, H - h)))
+        x0 = int(rng.integers(0, max(1, W - w)))
+        u1[y0:y0 + h, x0:x0 + w] = rng.uniform(-max_flow, max_flow - 1)
+        u2[y0:y0 + h, x0:x0 + w] = rng.uniform(-max_flow, max_flow - 1)
+    u1 = np.clip(np.rint(u1), -max_flow, max_flow - 1).astype(np.int64)
+    u2 = np.clip(np.rint(u2), -max_flow, max_flow - 1).astype(np.int64)
+    t = np.clip(tex, 0, 255)
+    i1 = t[pad + ys + u2, pad + xs + u1]
+    i2 = t[pad:pad + H, pad:pad + W]
+    i1 = np.clip(i1 + rng.normal(0, 2, size=(H, W)), 0, 255).astype(np.uint8)
+    i2 = np.clip(i2 + rng.normal(0, 2, size=(H, W)), 0, 255).astype(np.uint8)
+    return i1, i2, u1.astype(np.int32), u2.astype(np.int32)
+
+
 # Named configurations of BASELINE.json "configs" (SURVEY 8 table).
 CONFIGS = {
     "C1": dict(W=64, H=48, K=16, d_min=0, iters=5, kind="rd"),
     "C2": dict(W=1242, H=375, K=128, d_min=0, iters=4, kind="wt-kitti"),
     "C3": dict(W=1500, H=1000, K=256, d_min=0, iters=4, kind="wt-middlebury"),
+    # configs[3]: optical flow, discrete stage: 32 x 32 label window (u1, u2 in [-16, 15]),
+    # decoupled into two K = 32 layers (Eq. flow-decoupled-costs P:163-170)
+    "C4": dict(W=1242, H=375, K=32, d_min=-16, iters=4, kind="flow"),
     # configs[4]: a stream of 64 KITTI-shaped pairs, frames sharded over the GPUs
     "C5": dict(W=1242, H=375, K=128, d_min=0, iters=4, kind="wt-kitti", frames=64),
 }

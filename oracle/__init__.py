@@ -44,6 +44,7 @@ def _load():
         i32, i64 = ctypes.c_int, ctypes.c_int64
         lib.oracle_census.argtypes = [P, i32, i32, i32, P]
         lib.oracle_cost_volume.argtypes = [P, P, i32, i32, i32, i32, i32, P]
+        lib.oracle_flow_costs.argtypes = [P, P, i32, i32, i32, i32, i32, i32, i32, P, P]
         lib.oracle_msg_direct.argtypes = [P, i32, i64, i32, P]
         lib.oracle_msg.argtypes = [P, i32, i64, i32, P]
         lib.oracle_min_marginals.argtypes = [P, i32, i32, i64, i32, P]
@@ -81,6 +82,18 @@ def cost_volume(cl, cr, d_min: int, K: int, oob: int = 12) -> np.ndarray:
     if _load().oracle_cost_volume(_p(cl), _p(cr), W, H, d_min, K, oob, _p(D)):
         raise ValueError("oracle_cost_volume: bad arguments")
     return D
+
+
+def flow_costs(c1, c2, u1_min: int, K1: int, u2_min: int, K2: int, oob: int = 12):
+    """Optimistic decoupled flow costs (Eq. flow-decoupled-costs):
+    returns (f1 [H][W][K1], f2 [H][W][K2])."""
+    c1, c2 = _c(c1, np.uint32), _c(c2, np.uint32)
+    H, W = c1.shape
+    f1 = np.zeros((H, W, K1), np.uint8)
+    f2 = np.zeros((H, W, K2), np.uint8)
+    if _load().oracle_flow_costs(_p(c1), _p(c2), W, H, u1_min, K1, u2_min, K2, oob, _p(f1), _p(f2)):
+        raise ValueError("oracle_flow_costs: bad arguments")
+    return f1, f2
 
 
 def msg(a, ws: int, T: int, direct: bool = False) -> np.ndarray:

@@ -73,6 +73,34 @@ int oracle_cost_volume(const uint32_t* cl, const uint32_t* cr, int W, int H,
     return 0;
 }
 
+/* Eq. flow-decoupled-costs: the 2-D data cost D_i(x_i1, x_i2)
+ * of the flow label pair is reduced to one optimistic cost per layer by a
+ * minimum over the other layer's label.  Plain enumeration, K1*K2 Hamming
+ * distances per pixel. */
+int oracle_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int u1_min, int K1,
+                      int u2_min, int K2, int oob, uint8_t* f1, uint8_t* f2) {
+    if (!c1 || !c2 || !f1 || !f2 || W < 1 || H < 1 || K1 < 1 || K2 < 1 || K1 > 256 || K2 > 256 || oob < 0 ||
+        oob > 255)
+        return 1;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            uint8_t* o1 = f1 + ((size_t)y * W + x) * K1;
+            uint8_t* o2 = f2 + ((size_t)y * W + x) * K2;
+            for (int a = 0; a < K1; ++a) o1[a] = 255;
+            for (int b = 0; b < K2; ++b) o2[b] = 255;
+            for (int a = 0; a < K1; ++a)
+                for (int b = 0; b < K2; ++b) {
+                    const int xs = x + u1_min + a, ys = y + u2_min + b;
+                    const int d = (xs >= 0 && xs < W && ys >= 0 && ys < H)
+                                      ? popcount32(c1[(size_t)y * W + x] ^ c2[(size_t)ys * W + xs])
+                                      : oob;
+                    if (d < o1[a]) o1[a] = (uint8_t)d;
+                    if (d < o2[b]) o2[b] = (uint8_t)d;
+                }
+        }
+    return 0;
+}
+
 /* ------------------------------------------------------------- messages */
 /* Eq. msg-pass, Msg_ij of Alg.5:
  * phi(x_j) = min_{x_i} [a(x_i) + f_ij(x_i, x_j)], by enumeration. */

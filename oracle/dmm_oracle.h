@@ -39,6 +39,17 @@ int oracle_census(const uint8_t* img, int W, int H, int r, uint32_t* codes);
 int oracle_cost_volume(const uint32_t* cl, const uint32_t* cr, int W, int H,
                        int d_min, int K, int oob, uint8_t* D);
 
+/* Optimistic decoupled flow costs (Eq. "flow decoupled costs", P:163-170;
+ * Sec. 3.2 P:442-447 "decoupled into two independent stereo-like problems"),
+ * by plain enumeration of the 2-D label window: with displacements
+ * u1(a) = u1_min + a (a < K1, horizontal) and u2(b) = u2_min + b (b < K2,
+ * vertical), D(a,b) = popcount(c1[y][x] ^ c2[y+u2(b)][x+u1(a)]) or oob when
+ * the displaced pixel leaves the image (readings R22, R23), and
+ *   f1[y][x][a] = min_b D(a,b),   f2[y][x][b] = min_a D(a,b).
+ * f1 is [H][W][K1], f2 is [H][W][K2].  Returns 0 / 1 (bad args). */
+int oracle_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int u1_min, int K1,
+                      int u2_min, int K2, int oob, uint8_t* f1, uint8_t* f2);
+
 /* Message passing, definition (P:663-667 Eq. msg-pass; Msg in Alg.5):
  * out(b) = min_a a(a) + ws*min(|a-b|, T), by direct O(K^2) enumeration. */
 void oracle_msg_direct(const int64_t* a, int K, int64_t ws, int T, int64_t* out);
