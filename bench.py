@@ -197,7 +197,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)   # ~0.5 s timed: several nvidia-smi clock samples
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C5"),
+    ap.add_argument("--config", default="C2", choices=("C1", "C2", "C3", "C4", "C5"),
                     help="C2 (default): one KITTI frame per GPU per step; C5: configs[4], 64 KITTI frames per "
                          "step sharded over the GPUs, each GPU solving its frames as one batch (throughput mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -227,6 +227,8 @@ def main():
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
     if args.mode == "bands":
         return run_bands(args, c, world, rank, local, dev)
+    if c["kind"] == "flow":
+        return run_flow(args, c, world, rank, local, dev)
     total_frames = c.get("frames", world)          # C2: one frame per rank; C5: 64 frames per step
     nf = (total_frames + world - 1) // world
     distinct = [datagen.pair(c["kind"], W, H, K, seed=rank * nf + s) for s in range(min(nf, 8))]
@@ -379,6 +381,125 @@ def main():
             "clocks": clocks,
             "gpu_launches": launches,
             "result": {"energy": e / (1 << FBITS), "bound": b / (1 << FBITS)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_flow(args, c, world, rank, local, dev):
+    """configs[3] (C4), discrete stage of optical flow: census + the fused
+    32x32-window decoupled-cost kernel (Eq. flow-decoupled-costs)
+    + Dual MM on both K=32 layers (two frames of one context, same launches).
+    One frame pair per GPU (weak scaling).  cells = W*H*(K1 + K2)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1601_06274_b200 as dmm
+    W, H, K, iters, u_min = c["W"], c["H"], c["K"], c["iters"], c["d_min"]
+    i1, i2, _, _ = datagen.flow_pair(W, H, -u_min, seed=rank)
+    ctx = dmm.Context(width=W, height=H, d_min=u_min, d_max=u_min + K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
+                      max_iters=iters, batch=2, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    t1, t2 = torch.from_numpy(i1).to(dev), torch.from_numpy(i2).to(dev)
+
+    def step():
+        ctx.flow_cost_volume(t1, t2, u_min, stream=stream)
+        ctx.solve(iters, frame=0, nframes=2, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count - launches0
+    clocks = sampler.stop()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    prof_steps = max(1, min(args.steps, 50))
+    ctx.read_profile()
+    ctx.set_profiling(True)
+    for i in range(prof_steps):
+        flush.fill_(i & 0xff)
+        step()
+    torch.cuda.synchronize(dev)
+    ctx.set_profiling(False)
+    prof = ctx.read_profile()
+    cells = W * H * 2 * K
+    value = world * cells * iters / (ms / 1e3)
+    hbm, peak_kind = peaks()
+    hm_ms = (prof["hm_h"][0] + prof["hm_v"][0]) / prof_steps
+    alg = alg_bytes_compact(W, H, K, iters, 2)
+    flow_ms = prof["cost_volume"][0] / prof_steps
+    roofline = {"bound": "hbm", "achieved": alg / (hm_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": alg / (hm_ms / 1e3) / 1e9 / hbm, "traffic": traffic_per_half_step("C4"),
+                "kernel": "chain-DP half-step (root+level+leaf kernels), H and V, both flow layers",
+                "basis": "SURVEY 8(d) compact bytes of the two K=32 layers",
+                "peak_kind": peak_kind, "hm_ms_per_step": hm_ms, "profiled_steps": prof_steps,
+                "flow_cost_kernel": {"ms": flow_ms, "hamming_per_s": W * H * K * K / (flow_ms / 1e3),
+                                     "out_bytes_gbs": 2 * W * H * ctx.cost_volume_tensor(0).shape[2] /
+                                     (flow_ms / 1e3) / 1e9},
+                "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    # end to end through the public API with host buffers: H2D of both images,
+    # flow costs, both layers' Dual MM, D2H of both labellings
+    h1 = torch.from_numpy(i1).pin_memory()
+    h2 = torch.from_numpy(i2).pin_memory()
+    lab = torch.empty((2, H, W), dtype=torch.uint8).pin_memory()
+
+    def host_step():
+        t1.copy_(h1, non_blocking=True)
+        t2.copy_(h2, non_blocking=True)
+        step()
+        lab[0].copy_(ctx.labels(0, stream=stream), non_blocking=True)
+        lab[1].copy_(ctx.labels(1, stream=stream), non_blocking=True)
+
+    for _ in range(2):
+        host_step()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        host_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ems = max(e0.elapsed_time(e1) / args.steps, (time.perf_counter() - w0) * 1e3 / args.steps)
+    res = [ctx.result(f) for f in (0, 1)]
+    if rank == 0:
+        line = {
+            "metric": METRIC.replace("1242x375x128", "1242x375, 2 x 32 flow labels"), "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": f"C4: optical flow {W}x{H}, {K}x{K} label window (u in [{u_min}, {u_min + K - 1}]^2), "
+                                   f"decoupled into two {K}-label layers, {iters} dual iterations each, 1 pair per GPU",
+                       "W": W, "H": H, "K": K, "iters": iters, "fps": world / (ms / 1e3),
+                       "parallelism": f"frames x{world}",
+                       "l2": "flushed between timed steps (256 MB write outside events)"},
+            "roofline": roofline, "cpu_baseline": None,
+            "e2e": {"value": world * cells * iters / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * W * H,
+                    "d2h_bytes_per_step": 2 * W * H, "ms_per_step": ems},
+            "clocks": clocks, "gpu_launches": launches,
+            "result": {"energy": [r[0] / (1 << FBITS) for r in res], "bound": [r[1] / (1 << FBITS) for r in res]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

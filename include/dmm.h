@@ -140,6 +140,22 @@ DMM_API dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, con
                                        const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
                                        int64_t* energy, int64_t* bound, void* stream);
 
+/* Optical flow, discrete stage (NEXT-1; Eq. "flow decoupled costs"
+ * P:163-170, Sec. 3.2): census codes of both images into frame
+ * `frame`, then the optimistic decoupled costs of the 2-D label window
+ *   D(a,b) = popcount(c1(x,y) ^ c2(x + u1(a), y + u2(b))) (oob outside the image),
+ *   u1(a) = d_min + a (horizontal, the config's range), u2(b) = v_min + b (vertical),
+ *   f1(a) = min_b D(a,b) -> cost volume of frame `frame`,
+ *   f2(b) = min_a D(a,b) -> cost volume of frame `frame + 1`,
+ * by one fused kernel that never stores the K*K volume.  Note the sign: flow
+ * matches x + u (stereo matches x - d).  K = d_max - d_min + 1 must be 16, 32,
+ * 48 or 64 (both layers have K labels); frames frame, frame+1 < batch.  The
+ * two layers are then independent K-label problems ("two independent
+ * stereo-like problems"): dmm_solve(ctx, frame, 2, ...) solves both
+ * in the same launches; labels of frame / frame+1 are u1 - d_min / u2 - v_min. */
+DMM_API dmm_status dmm_flow_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right,
+                                        int64_t pitch, int32_t v_min, void* stream);
+
 /* ---- chain-DP primitives (no context; device int32 arrays, dense
  * [count][K], K in [1, 256], ws = w * 2^F >= 0, T >= 1).  They run exactly the
  * device code of the Dual MM kernels, one warp per K-vector.

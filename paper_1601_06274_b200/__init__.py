@@ -28,7 +28,7 @@ EXPORTS = (
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
     "dmm_cost_volume_frames", "dmm_run_host_frames", "dmm_energy_of",
-    "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
+    "dmm_flow_cost_volume", "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
 )
 SHARD_FRAMES, SHARD_ROWCOL = 0, 1
 LOC_FV_H, LOC_FH_H, LOC_FV_V, LOC_FH_V, LOC_LABEL_V, LOC_BOUNDS = range(6)
@@ -103,6 +103,7 @@ def load_library():
         "dmm_half_step": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, i32, ctypes.c_int, i32, P]),
         "dmm_energy": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(i64), P]),
         "dmm_energy_of": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.POINTER(i64), P]),
+        "dmm_flow_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P, i64, i32, P]),
         "dmm_nccl_unique_id": (ctypes.c_int, [P]),
         "dmm_shard": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "dmm_shard_workspace_bytes": (ctypes.c_size_t, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -284,6 +285,22 @@ class Context:
             raise DmmError("left/right row pitch differ")
         self._call("dmm_cost_volume", frame, ctypes.c_void_p(left.data_ptr()),
                    ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream, self.device))
+
+    def flow_cost_volume(self, left, right, v_min: int, frame: int = 0, stream=None):
+        """Optical flow, discrete stage (dmm_flow_cost_volume): the decoupled
+        costs f1 (horizontal u1 = d_min + label) into frame `frame` and f2
+        (vertical u2 = v_min + label) into frame `frame + 1`; then
+        solve(iterations, frame, nframes=2) solves both layers."""
+        for t in (left, right):
+            if t.dtype.itemsize != 1 or t.device != self.device or t.dim() != 2 or t.stride(1) != 1:
+                raise DmmError("images must be uint8 (H, W) row-major tensors on the context device")
+            if tuple(t.shape) != (self.H, self.W):
+                raise DmmError(f"image shape {tuple(t.shape)} != {(self.H, self.W)}")
+        if left.stride(0) != right.stride(0):
+            raise DmmError("left/right row pitch differ")
+        self._call("dmm_flow_cost_volume", frame, ctypes.c_void_p(left.data_ptr()), ctypes.c_void_p(right.data_ptr()),
+                   left.stride(0), v_min, _stream_handle(stream, self.device))
+        self._iters[frame] = self._iters[frame + 1] = 0
 
     def cost_volume_frames(self, left, right, frame: int = 0, stream=None):
         """left/right: torch.uint8 (nframes, H, W) contiguous stacks on this device:

@@ -292,6 +292,29 @@ dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const u
     return DMM_OK;
 }
 
+dmm_status dmm_flow_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right, int64_t pitch,
+                                int32_t v_min, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
+    dmm_status st = frame_ok(ctx, frame, 2);
+    if (st || (st = not_sharded(ctx, "dmm_flow_cost_volume"))) return st;
+    if (!left || !right) { ctx->err = "null image"; return DMM_E_ARG; }
+    if (pitch < ctx->cfg.width) { ctx->err = "pitch < width"; return DMM_E_SHAPE; }
+    if (!dmm::flow_k_ok(ctx->K)) { ctx->err = "flow window: K must be 16, 32, 48 or 64"; return DMM_E_ARG; }
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    dmm::FramePtrs P2 = dmm::frame_ptrs(ctx->L, frame + 1);
+    { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, 1, ctx->cfg.census_radius, pitch, left, right, s); }
+    {
+        Timed t(ctx, 1, s);
+        dmm::launch_flow_costs(P.codes_l, P.codes_r, ctx->cfg.width, ctx->cfg.height, ctx->K, ctx->KP, ctx->cfg.d_min,
+                               v_min, ctx->oob, P.D, P2.D, s);
+    }
+    if ((st = check_launch(ctx, "flow cost volume"))) return st;
+    for (int f = frame; f < frame + 2; ++f) { ctx->has_cost[f] = 1; ctx->iters_done[f] = 0; }
+    return DMM_OK;
+}
+
 dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, void* stream) {
     if (!ctx) return DMM_E_ARG;
     DMM_DEVICE_GUARD(ctx);

@@ -113,6 +113,11 @@ void launch_hm2_pass(const PassArgs& a, int vertical, int nframes, cudaStream_t 
 int hm2_launches_per_pass(const PassArgs& a, int vertical);
 // labels == nullptr: the frames' own labels; else a caller labelling u8 [H][W]
 // (one frame); bad (nullable) is set to 1 if a label is >= K.
+// Optimistic decoupled flow costs (flow.cu): f1 -> D1 [H][W][KP], f2 -> D2;
+// K in {16, 32, 48, 64} (flow_k_ok).
+bool flow_k_ok(int K);
+void launch_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int K, int KP, int u1_min, int u2_min,
+                       int oob, uint8_t* D1, uint8_t* D2, cudaStream_t s);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    const uint8_t* labels, int32_t* bad, cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);

@@ -488,3 +488,58 @@ def test_partial_solve_has_no_result():
     ctx.set_stop_after_h(False)
     ctx.solve(2)
     assert ctx.result()[1] <= ctx.result()[0]
+
+
+# ------------------------------------------------------------ NEXT-1 flow
+def _flow_gpu(i1, i2, K, u1_min, u2_min, iters, **kw):
+    H, W = i1.shape
+    ctx = _ctx(width=W, height=H, d_min=u1_min, d_max=u1_min + K - 1, batch=2, max_iters=max(iters, 1), **kw)
+    ctx.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i2).cuda(), u2_min)
+    f1 = ctx.cost_volume_tensor(0).cpu().numpy()
+    f2 = ctx.cost_volume_tensor(1).cpu().numpy()
+    out = dict(f1=f1, f2=f2)
+    if iters:
+        ctx.solve(iters, frame=0, nframes=2)
+        for f in (0, 1):
+            e, b, h = ctx.result(f)
+            out[f] = dict(labels=ctx.labels(f).cpu().numpy().astype(np.int32), energy=e, hist=np.array(h, np.int64))
+    return out
+
+
+@pytest.mark.parametrize("W,H,K,u1,u2", [(77, 45, 32, -16, -16), (40, 70, 16, -3, -12), (131, 29, 64, -40, -20),
+                                         (33, 33, 48, 5, -60), (16, 9, 32, -16, -16)])
+def test_flow_costs_parity(orc, W, H, K, u1, u2):
+    """dmm_flow_cost_volume (fused 2-D window kernel) == oracle_flow_costs,
+    bit-exact: interior and border tiles, windows partly / wholly outside."""
+    i1, i2, _, _ = datagen.flow_pair(W, H, 16, seed=W + H)
+    g = _flow_gpu(i1, i2, K, u1, u2, 0)
+    of1, of2 = orc.flow_costs(orc.census(i1), orc.census(i2), u1, K, u2, K)
+    assert np.array_equal(g["f1"], of1)
+    assert np.array_equal(g["f2"], of2)
+
+
+def test_flow_c4_full_size(orc):
+    """configs[3] (C4) at full size: 1242x375, 32x32 window, both layers' Dual MM
+    (4 iterations, solved as two frames of one context) bit-exact vs the oracle."""
+    c = datagen.CONFIGS["C4"]
+    W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+    i1, i2, _, _ = datagen.flow_pair(W, H, 16, seed=0)
+    g = _flow_gpu(i1, i2, K, -16, -16, iters)
+    of1, of2 = orc.flow_costs(orc.census(i1), orc.census(i2), -16, K, -16, K)
+    assert np.array_equal(g["f1"], of1) and np.array_equal(g["f2"], of2)
+    for f, D in ((0, of1), (1, of2)):
+        o = orc.dmm(D, 3, 3, 4, 4, iters, nthreads=16)
+        assert np.array_equal(g[f]["labels"], o["labels"])
+        assert np.array_equal(g[f]["hist"], o["bound_hist"])
+        assert g[f]["energy"] == o["energy"]
+
+
+def test_flow_rejects_bad_window():
+    import paper_1601_06274_b200 as dmm
+    i1 = np.zeros((20, 30), np.uint8)
+    ctx = _ctx(width=30, height=20, d_min=0, d_max=19, batch=2)
+    with pytest.raises(dmm.DmmError):
+        ctx.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i1).cuda(), 0)
+    ctx1 = _ctx(width=30, height=20, d_min=0, d_max=15, batch=1)
+    with pytest.raises(dmm.DmmError):
+        ctx1.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i1).cuda(), 0)
