@@ -26,6 +26,10 @@ template <int LPL> constexpr int nwg() { return 2; }   // warps per CTA, level k
 constexpr int kNWL = 8;      // warps per CTA, leaf kernel
 constexpr int kRootCH = 16, kRootNS = 2;
 constexpr int kLevCH = 8, kLevNS = 2;
+#ifndef DMM_LEV_MIN_CTAS
+#define DMM_LEV_MIN_CTAS 12
+#endif
+constexpr int kLevMinCTAs = DMM_LEV_MIN_CTAS;   // 2-warp level CTAs per SM the register budget must allow
 static_assert(kRootCH <= 16 && kLevCH <= 16, "pair_range_ok (capi.cu) allows 16 unnormalised steps");
 
 __host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
@@ -241,19 +245,26 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         const int len0 = nsteps + 1;
         int kk = DIR > 0 ? (31 - __clz(len0)) - 1 : 31 - __clz(len0 - 1);
         int target = DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1);
-        unsigned G = 0u;      // min of the current phi.m (packed)
+        unsigned G = 0u;      // min of the current phi (packed)
         int gA = 0, gB = 0;
+        // phi = min(phi.m, cap): the truncation cap of the last Msg is applied
+        // lazily (dt2_min / dt2_window), so the step's warp reduction overlaps
+        // the window pass; kBigP = no pending cap
+        unsigned cap = kBigP;
         auto normalise = [&]() {
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) phi.m[e] = __vsub2(phi.m[e], G);
+            for (int e = 0; e < LPL; ++e) phi.m[e] = __vsub2(__vmins2(phi.m[e], cap), G);
             phi.a += gA; phi.b += gB;
             G = 0u; gA = 0; gB = 0;
+            cap = kBigP;
         };
         auto step = [&](const unsigned (&v)[LPL], int ba, int bb) {
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) phi.m[e] += v[e];     // both >= 0 per half: no carry
+            for (int e = 0; e < LPL; ++e) phi.m[e] = __vmins2(phi.m[e], cap) + v[e];   // halves >= 0: no carry
             phi.a += ba; phi.b += bb;
-            G = dtrans2<LPL, PAD, WIN, false>(phi.m, this->dk, gA, gB);
+            G = dt2_min<LPL, PAD>(phi.m, this->dk, gA, gB);
+            dt2_window<LPL, WIN>(phi.m, this->dk);
+            cap = __vadd2(G, this->dk.capP);
         };
         auto spine = [&](int s) {
             if (s + 2 == target) {
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(64) hm2_root_kernel(PassArgs a) {
 }
 
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int NW>
-__global__ void __launch_bounds__(NW * 32, 12) hm2_level_kernel(PassArgs a, int lev, int ntasks) {
+__global__ void __launch_bounds__(NW * 32, kLevMinCTAs) hm2_level_kernel(PassArgs a, int lev, int ntasks) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int KP = 32 * LPL;
