@@ -1,0 +1,157 @@
+"""Continuous refinement oracle (NEXT-2 of SURVEY 8(f)): the non-convex
+primal-dual refinement of a discrete stereo labelling, Sec. 2.4
+and Sec. 3.1 of arXiv 1601.06274.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py): only tests/, smoke() and
+bench.py's cpu_baseline / reference legs may import it.  Plain numpy, float64,
+one function per step of the method in the paper's order and notation; no
+fusion or reordering beyond what the iterates state.
+
+Problem (Eq. compact_formulation): min_u D(u) + R(Au), with
+  (Au)_ij = u_i - u_j over the 4-connected edges,
+  R(Au) = sum_ij w_ij r((Au)_ij)  (Eq. regularizer-form),
+  r = r_{eps,delta} - r_{0, C + delta - eps*delta}  (Eq. r-decompose),
+  r_{a,b}(t) = a|t| if |t| <= b else |t| - b(1 - a).
+Iterates (Eq. cont_iterates) on x = (u, q), y = (p, d = 1) with
+A(x) = [Au; -<Au, q>], G(x) = R_-^*(q) + D~(u), F^*(y) = R_+^*(p),
+grad A(x) = [[A, 0], [-A^T q, -Au]]:
+  u+ = prox_{tau D~}(u - tau A^T (p - q))
+  q+ = prox_{tau R_-^*}(q + tau A u)
+  p+ = prox_{sigma R_+^*}(p + sigma A(2 u+ - u))
+Prox of (w r_{a,b})^* (Eq. pprox): t' = t if |t| <= a w else
+sign(t) max(a w, |t| - b * step), then clamp to [-w, w].
+Data term: the two-slope convex approximation around the current
+point, with the indicator of [u0 - h, u0 + h]; its prox; embedded in
+a warping loop: `warps` re-approximations x `iters` iterations
+(5 x 40 in the paper's timing run).
+
+Readings of garbled / silent passages (R24-R28):
+  R24 slopes: s1 = (D(u0) - D(u0 - h)) / h (left), s2 = (D(u0 + h) - D(u0)) / h
+      (right); P:427's s2 = (D(u0) - D(u0+h))/h is -s1, a typo; "set s1 = s2 =
+      (s1+s2)/2 if s2 < s1" then makes the function convex.
+  R25 data prox: the exact prox of the two-slope function (kink at u0 maps to
+      u0 in the middle case, P:434-440 prints "u^ - 0"), then the clamp.
+  R26 D at a real label u: linear interpolation of the sampled cost volume,
+      u clamped to [0, K-1] for the lookup.
+  R27 constants: h = 1 label, tau = sigma = 0.35 (tau*sigma*||A||^2 < 1,
+      ||A||^2 <= 8), p = q = 0 at the start and kept across warps, u starts at
+      the discrete labelling; eps, delta, C, w from the caller (eps = 1,
+      C = T, w = w_h / w_v reproduces the discrete truncated-linear model).
+  R28 the conjugate's domain "alpha < |t*| < omega" is read as
+      |t*| <= omega (value beta * max(0, |t*| - alpha*omega)), whose prox is
+      P:390-397 exactly.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+# ------------------------------------------------------------ regulariser
+def r_ab(t, a: float, b: float):
+    """r_{a,b}(t)."""
+    t = np.abs(np.asarray(t, np.float64))
+    return np.where(t <= b, a * t, t - b * (1.0 - a))
+
+
+def r_dc(t, eps: float, delta: float, C: float):
+    """r = r_{eps,delta} - r_{0, C + delta - eps*delta} (Eq. r-decompose)."""
+    return r_ab(t, eps, delta) - r_ab(t, 0.0, C + delta - eps * delta)
+
+
+def conj_w_rab(s, w: float, a: float, b: float):
+    """(w r_{a,b})^*(s) (reading R28): b * max(0, |s| - a w) on |s| <= w, +inf outside."""
+    s = np.abs(np.asarray(s, np.float64))
+    return np.where(s <= w + 1e-12, b * np.maximum(0.0, s - a * w), np.inf)
+
+
+def prox_conj(t, w, a: float, b: float, step: float):
+    """Prox of step * (w r_{a,b})^* (Eq. pprox), componentwise."""
+    t = np.asarray(t, np.float64)
+    aw = a * w
+    tp = np.where(np.abs(t) <= aw, t, np.sign(t) * np.maximum(aw, np.abs(t) - b * step))
+    return np.clip(tp, -w, w)
+
+
+# ---------------------------------------------------------------- operator A
+def A(u):
+    """(Au)_ij = u_i - u_j: horizontal edges (y, x)-(y, x+1) and vertical
+    edges (y, x)-(y+1, x), each indexed by its first pixel."""
+    return u[:, :-1] - u[:, 1:], u[:-1, :] - u[1:, :]
+
+
+def AT(ph, pv, shape):
+    """Adjoint of A: node i gets +p_ij of its edges as first node, -p of the
+    edges where it is the second node."""
+    out = np.zeros(shape, np.float64)
+    out[:, :-1] += ph
+    out[:, 1:] -= ph
+    out[:-1, :] += pv
+    out[1:, :] -= pv
+    return out
+
+
+# ------------------------------------------------------------------ data
+def D_interp(D, u):
+    """D at a real label u (reading R26): linear interpolation between labels."""
+    H, W, K = D.shape
+    uc = np.clip(u, 0.0, K - 1.0)
+    k0 = np.minimum(np.floor(uc).astype(np.int64), K - 1)
+    k1 = np.minimum(k0 + 1, K - 1)
+    f = uc - k0
+    yy, xx = np.mgrid[0:H, 0:W]
+    d0 = D[yy, xx, k0].astype(np.float64)
+    d1 = D[yy, xx, k1].astype(np.float64)
+    return (1.0 - f) * d0 + f * d1
+
+
+def slopes(D, u0, h: float):
+    """Two-slope convex approximation around u0 (reading R24)."""
+    s1 = (D_interp(D, u0) - D_interp(D, u0 - h)) / h
+    s2 = (D_interp(D, u0 + h) - D_interp(D, u0)) / h
+    avg = 0.5 * (s1 + s2)
+    bad = s2 < s1
+    return np.where(bad, avg, s1), np.where(bad, avg, s2)
+
+
+def prox_data(uh, u0, s1, s2, tau: float, h: float):
+    """Prox of tau * D~ (reading R25): soft threshold towards the
+    kink u0 with the left / right slopes, then clamp to [u0 - h, u0 + h]."""
+    v = np.where(uh > u0 + tau * s2, uh - tau * s2, np.where(uh < u0 + tau * s1, uh - tau * s1, u0))
+    return np.clip(v, u0 - h, u0 + h)
+
+
+# ---------------------------------------------------------------- energy
+def energy(D, u, w_h: float, w_v: float, eps: float, delta: float, C: float):
+    """E(u) = D(u) + R(Au) (Eq. mrf_formulation, regularizer-form P:134)."""
+    ah, av = A(u)
+    return float(D_interp(D, u).sum() + w_h * r_dc(ah, eps, delta, C).sum() + w_v * r_dc(av, eps, delta, C).sum())
+
+
+# ------------------------------------------------------------ the method
+def refine(D, labels, w_h: float, w_v: float, eps: float = 1.0, delta: float = 1.0, C: float = 4.0,
+           h: float = 1.0, tau: float = 0.35, sigma: float = 0.35, warps: int = 5, iters: int = 40):
+    """Refine a discrete labelling (label units) of cost volume D [H][W][K].
+    Returns the real-valued labelling u [H][W] (label units; disparity =
+    d_min + u) and its energy."""
+    D = np.asarray(D)
+    H, W, K = D.shape
+    u = np.asarray(labels, np.float64).copy()
+    ph = np.zeros((H, W - 1)); pv = np.zeros((H - 1, W))
+    qh = np.zeros((H, W - 1)); qv = np.zeros((H - 1, W))
+    bp = C + delta - eps * delta                      # beta of R_-
+    for _ in range(warps):
+        u0 = u.copy()
+        s1, s2 = slopes(D, u0, h)
+        for _ in range(iters):
+            # x^{k+1} = (I + tau dG)^{-1}(x^k - tau [grad A(x^k)]^T y^k), d = 1
+            uh = u - tau * AT(ph - qh, pv - qv, (H, W))
+            u_new = prox_data(uh, u0, s1, s2, tau, h)
+            ah, av = A(u)
+            qh = prox_conj(qh + tau * ah, w_h, 0.0, bp, tau)
+            qv = prox_conj(qv + tau * av, w_v, 0.0, bp, tau)
+            # y^{k+1} = (I + sigma dF^*)^{-1}(y^k + sigma A(2 x^{k+1} - x^k))
+            bh, bv = A(2.0 * u_new - u)
+            ph = prox_conj(ph + sigma * bh, w_h, eps, delta, sigma)
+            pv = prox_conj(pv + sigma * bv, w_v, eps, delta, sigma)
+            u = u_new
+    return u, energy(D, u, w_h, w_v, eps, delta, C)
