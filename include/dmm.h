@@ -140,6 +140,31 @@ DMM_API dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, con
                                        const uint8_t* right_host, int32_t iterations, uint8_t* labels_host,
                                        int64_t* energy, int64_t* bound, void* stream);
 
+/* Continuous refinement of the frame's labelling (NEXT-2; Sec. 2.4 P:283-405,
+ * Sec. 3.1): the non-convex primal-dual iterates (Eq.
+ * cont_iterates P:306-311, Valkonen's PDHG on the DC split
+ * r = r_{eps,delta} - r_{0,C+delta-eps*delta}, Eq. r-decompose P:364-375,
+ * prox Eq. pprox) on the two-slope convex approximation of the
+ * data term around the current solution, re-approximated
+ * `warps` times with `iters` iterations each (5 x 40 in P:497).
+ * Weights w_h / w_v of the config; float32 on the device.  Readings
+ * R24-R28: h in label units, linear interpolation of D between
+ * labels, tau * sigma * 8 < 1 for convergence (0.35 / 0.35 suggested).
+ * eps = 1, C = trunc gives the discrete model's truncated-linear r.
+ * u_out (nullable): device float [H][W], refined disparity (d_min + label
+ * units).  energy (nullable, host): E(u) = D(u) + R(Au), double; if given the
+ * call synchronises `stream`.  DMM_E_STATE before dmm_solve.  The iterations
+ * of one warp are captured once into a CUDA graph (per frame and parameters)
+ * and replayed. */
+typedef struct dmm_refine_params {
+    float eps, delta, C;      /* penalty r: slope eps up to delta, slope 1, truncated at C  */
+    float h;                  /* data approximation step / trust region (labels)          */
+    float tau, sigma;         /* primal / dual step sizes                                   */
+    int32_t warps, iters;     /* re-approximations x PDHG iterations each                   */
+} dmm_refine_params;
+DMM_API dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* u_out, double* energy,
+                              void* stream);
+
 /* Optical flow, discrete stage (NEXT-1; Eq. "flow decoupled costs"
  * P:163-170, Sec. 3.2): census codes of both images into frame
  * `frame`, then the optimistic decoupled costs of the 2-D label window
@@ -279,8 +304,9 @@ DMM_API int64_t dmm_launch_count(const dmm_ctx* ctx);
  * around every kernel (enable != 0).  dmm_read_profile synchronises the
  * recorded events, writes per-class totals (ms[c], launches[c]) for the
  * classes c = 0 census, 1 cost volume, 2 H half-step, 3 V half-step,
- * 4 energy (arrays of DMM_PROFILE_CLASSES entries) and clears the record. */
-#define DMM_PROFILE_CLASSES 5
+ * 4 energy, 5 continuous refinement (arrays of DMM_PROFILE_CLASSES entries)
+ * and clears the record. */
+#define DMM_PROFILE_CLASSES 6
 DMM_API dmm_status dmm_set_profiling(dmm_ctx* ctx, int enable);
 DMM_API dmm_status dmm_read_profile(dmm_ctx* ctx, double* ms, int64_t* launches);
 

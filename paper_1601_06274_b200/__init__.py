@@ -28,7 +28,7 @@ EXPORTS = (
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
     "dmm_cost_volume_frames", "dmm_run_host_frames", "dmm_energy_of",
-    "dmm_flow_cost_volume", "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
+    "dmm_flow_cost_volume", "dmm_refine", "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
 )
 SHARD_FRAMES, SHARD_ROWCOL = 0, 1
 LOC_FV_H, LOC_FH_H, LOC_FV_V, LOC_FH_V, LOC_LABEL_V, LOC_BOUNDS = range(6)
@@ -36,7 +36,7 @@ BUF_D, BUF_FV, BUF_FH, BUF_LABELS, BUF_BOUNDS = 0, 1, 2, 3, 4
 TUNE_STOP_AFTER_H = 2
 TUNE_PAIR = 3
 TUNE_QUERY_PAIR = 4
-PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy")
+PROFILE_CLASSES = ("census", "cost_volume", "hm_h", "hm_v", "energy", "refine")
 
 
 class DmmError(RuntimeError):
@@ -47,6 +47,12 @@ class DmmConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "width", "height", "d_min", "d_max", "census_radius", "w_h", "w_v", "trunc",
         "frac_bits", "oob_cost", "batch", "max_iters")]
+
+
+class DmmRefineParams(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_float), ("delta", ctypes.c_float), ("C", ctypes.c_float), ("h", ctypes.c_float),
+                ("tau", ctypes.c_float), ("sigma", ctypes.c_float), ("warps", ctypes.c_int32),
+                ("iters", ctypes.c_int32)]
 
 
 class DmmXfer(ctypes.Structure):
@@ -104,6 +110,8 @@ def load_library():
         "dmm_energy": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(i64), P]),
         "dmm_energy_of": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.POINTER(i64), P]),
         "dmm_flow_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P, i64, i32, P]),
+        "dmm_refine": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(DmmRefineParams), P,
+                                      ctypes.POINTER(ctypes.c_double), P]),
         "dmm_nccl_unique_id": (ctypes.c_int, [P]),
         "dmm_shard": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "dmm_shard_workspace_bytes": (ctypes.c_size_t, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -285,6 +293,20 @@ class Context:
             raise DmmError("left/right row pitch differ")
         self._call("dmm_cost_volume", frame, ctypes.c_void_p(left.data_ptr()),
                    ctypes.c_void_p(right.data_ptr()), left.stride(0), _stream_handle(stream, self.device))
+
+    def refine(self, eps: float = 1.0, delta: float = 1.0, C: float | None = None, h: float = 1.0,
+               tau: float = 0.35, sigma: float = 0.35, warps: int = 5, iters: int = 40, frame: int = 0,
+               stream=None, energy: bool = True):
+        """Continuous refinement (dmm_refine) of the frame's labelling; returns
+        (u, energy): u = torch.float32 (H, W) refined disparities on the device,
+        energy = E(u) (float, or None if energy=False).  C defaults to T."""
+        import torch
+        prm = DmmRefineParams(eps, delta, float(self.cfg.trunc if C is None else C), h, tau, sigma, warps, iters)
+        out = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+        e = ctypes.c_double()
+        self._call("dmm_refine", frame, ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
+                   ctypes.byref(e) if energy else None, _stream_handle(stream, self.device))
+        return out, (float(e.value) if energy else None)
 
     def flow_cost_volume(self, left, right, v_min: int, frame: int = 0, stream=None):
         """Optical flow, discrete stage (dmm_flow_cost_volume): the decoupled

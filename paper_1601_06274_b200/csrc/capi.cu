@@ -90,6 +90,8 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->bounds = (long long*)take(8 * 2 * (size_t)c->max_iters);
     off->energy = (long long*)take(8);
     off->flag = (int32_t*)take(8);
+    off->rf = (float*)take(dmm::refine_bytes((int)W, (int)H));
+    off->renergy = (double*)take(8);
     return o;
 }
 
@@ -241,6 +243,8 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.bounds = (long long*)(b + (size_t)off.bounds);
     c->L.base.energy = (long long*)(b + (size_t)off.energy);
     c->L.base.flag = (int32_t*)(b + (size_t)off.flag);
+    c->L.base.rf = (float*)(b + (size_t)off.rf);
+    c->L.base.renergy = (double*)(b + (size_t)off.renergy);
     c->L.W = cfg->width; c->L.H = cfg->height; c->L.K = c->K; c->L.KP = c->KP;
     c->ws = b;
     c->ws_bytes = bytes;
@@ -265,6 +269,7 @@ void dmm_destroy(dmm_ctx* ctx) {
     for (auto& r : ctx->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto e : ctx->pool) cudaEventDestroy(e);
     dmm::shard_release(ctx);
+    dmm::refine_release(ctx);
     delete[] ctx->has_cost;
     delete[] ctx->iters_done;
     delete ctx;
@@ -289,6 +294,32 @@ dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const u
     if ((st = check_launch(ctx, "cost_volume"))) return st;
     ctx->has_cost[frame] = 1;
     ctx->iters_done[frame] = 0;
+    return DMM_OK;
+}
+
+dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* u_out, double* energy,
+                      void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
+    dmm_status st = frame_ok(ctx, frame);
+    if (st || (st = not_sharded(ctx, "dmm_refine"))) return st;
+    if (!prm || prm->warps < 0 || prm->iters < 0 || prm->iters > 4096 || !(prm->h > 0.f) || !(prm->tau > 0.f) ||
+        !(prm->sigma > 0.f) || !(prm->eps >= 0.f && prm->eps <= 1.f) || !(prm->delta >= 0.f) || !(prm->C >= 0.f)) {
+        ctx->err = "bad refinement parameters";
+        return DMM_E_ARG;
+    }
+    if (ctx->iters_done[frame] < 1) { ctx->err = "refine before solve (needs the discrete labelling)"; return DMM_E_STATE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    if (energy && (st = cuda_err(ctx, cudaMemsetAsync(P.renergy, 0, 8, s), "memset"))) return st;
+    {
+        Timed t(ctx, 5, s, 0);
+        if ((st = dmm::refine_run(ctx, frame, prm, u_out, energy ? P.renergy : nullptr, s))) return st;
+    }
+    if (energy) {
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(energy, P.renergy, 8, cudaMemcpyDeviceToHost, s), "d2h"))) return st;
+        if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
+    }
     return DMM_OK;
 }
 

@@ -28,6 +28,16 @@ struct ShardState {
     long long* bounds = nullptr;      // [2*max_iters] then energy: one all-reduce
 };
 
+// The captured CUDA graph of one refinement warp (refine.cu), cached per
+// (frame, parameters).
+struct RefineGraph {
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cap = nullptr;
+    int frame = -1;
+    dmm_refine_params prm{};
+    float* rf = nullptr;
+};
+
 struct dmm_ctx {
     dmm_config cfg;
     int K, KP, device, oob;
@@ -48,6 +58,7 @@ struct dmm_ctx {
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     ShardState sh;
+    RefineGraph rg;
 };
 
 namespace dmm {
@@ -62,4 +73,9 @@ dmm_status shard_cost_volume(dmm_ctx* ctx, const uint8_t* left, const uint8_t* r
 dmm_status shard_solve(dmm_ctx* ctx, int iterations, cudaStream_t s);
 dmm_status shard_half_step(dmm_ctx* ctx, int t, int vertical, int iterations, cudaStream_t s);
 void shard_release(dmm_ctx* ctx);
+// refine.cu
+size_t refine_bytes(int W, int H);
+dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,
+                      cudaStream_t s);
+void refine_release(dmm_ctx* ctx);
 }  // namespace dmm

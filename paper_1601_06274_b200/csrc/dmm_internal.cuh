@@ -44,6 +44,8 @@ struct FramePtrs {
     long long* bounds;   // [2 * max_iters]
     long long* energy;   // [1]
     int32_t* flag;       // [1] scratch: label-range flag of dmm_energy_of
+    float* rf;           // continuous refinement state (refine.cu): 11 x float [H][W]
+    double* renergy;     // [1] energy of the refined labelling
 };
 
 // Per-frame pointers are base + frame * stride (bytes).
@@ -72,6 +74,8 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.bounds = (long long*)((char*)p.bounds + o);
     p.energy = (long long*)((char*)p.energy + o);
     p.flag = (int32_t*)((char*)p.flag + o);
+    p.rf = (float*)((char*)p.rf + o);
+    p.renergy = (double*)((char*)p.renergy + o);
     return p;
 }
 

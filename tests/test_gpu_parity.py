@@ -543,3 +543,49 @@ def test_flow_rejects_bad_window():
     ctx1 = _ctx(width=30, height=20, d_min=0, d_max=15, batch=1)
     with pytest.raises(dmm.DmmError):
         ctx1.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i1).cuda(), 0)
+
+
+# ------------------------------------------------- NEXT-2 continuous refinement
+REFINE_U_TOL = 1e-3       # labels; derivation in DESIGN.md "Continuous refinement: float32 tolerance"
+REFINE_E_RTOL = 1e-5
+
+
+@pytest.mark.parametrize("W,H,K,eps,delta,C,warps,iters", [(96, 40, 32, 1.0, 1.0, 4.0, 5, 40),
+                                                           (61, 23, 48, 0.5, 2.0, 5.0, 3, 25),
+                                                           (33, 17, 16, 0.25, 1.0, 3.0, 2, 7)])
+def test_refine_parity(orc, W, H, K, eps, delta, C, warps, iters):
+    """dmm_refine (float32, CUDA graph of the PDHG iterations) vs the float64
+    oracle (oracle/refine.py) started from the same discrete labelling."""
+    from oracle import refine as orf
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=W)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=4)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(4)
+    u, e = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    D = ctx.cost_volume_tensor().cpu().numpy()
+    lab = ctx.labels().cpu().numpy()
+    uo, eo = orf.refine(D, lab, 3.0, 3.0, eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    du = np.abs(u.cpu().numpy().astype(np.float64) - uo)
+    print(f"refine max |du| = {du.max():.3e}, energy {e:.6f} vs {eo:.6f} (rel {abs(e - eo) / abs(eo):.2e})")
+    assert du.max() <= REFINE_U_TOL
+    assert abs(e - eo) <= REFINE_E_RTOL * abs(eo) + 1e-3
+    # a second call with the same parameters replays the cached graph: same result
+    u2, e2 = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    assert torch.equal(u, u2) and e2 == e
+
+
+def test_refine_c2_full_size(orc):
+    """configs[1] shape: DMM (4 iterations) then 5 x 40 refinement iterations
+    (the paper's timing run), float32 vs the float64 oracle."""
+    from oracle import refine as orf
+    c = datagen.CONFIGS["C2"]
+    W, H, K = c["W"], c["H"], c["K"]
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=0)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=4)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(4)
+    u, e = ctx.refine()
+    uo, eo = orf.refine(ctx.cost_volume_tensor().cpu().numpy(), ctx.labels().cpu().numpy(), 3.0, 3.0, C=4.0)
+    du = np.abs(u.cpu().numpy().astype(np.float64) - uo)
+    assert du.max() <= REFINE_U_TOL, du.max()
+    assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
