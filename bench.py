@@ -202,6 +202,9 @@ def main():
                          "step sharded over the GPUs, each GPU solving its frames as one batch (throughput mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--refine", action="store_true",
+                    help="append the continuous refinement (NEXT-2: 5 warps x 40 PDHG iterations, P:497) to every "
+                         "step (frames mode, one frame per GPU)")
     ap.add_argument("--mode", choices=("frames", "bands"), default="frames",
                     help="frames: one frame per GPU (weak scaling); bands: one frame sharded in row/column "
                          "bands with an all-to-all between half-steps (strong scaling)")
@@ -247,6 +250,9 @@ def main():
         else:
             ctx.cost_volume_frames(lt, rt, stream=stream)
         ctx.solve(iters, frame=0, nframes=nf, stream=stream)
+        if args.refine:
+            for f in range(nf):
+                ctx.refine(frame=f, stream=stream, energy=False)
 
     for _ in range(args.warmup):
         step()
@@ -317,6 +323,14 @@ def main():
                 "traffic_source": f"profiles/ncu_traffic_{args.config}.json" if tr else None,
                 "share_of_step": hm_ms_per_step / step_ms_prof if step_ms_prof else None,
                 "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    refine = None
+    if args.refine:
+        rms = prof["refine"][0] / prof_steps
+        # per PDHG iteration and pixel (one fused kernel, float64): reads u, u0, s1, s2, p_h, p_v,
+        # q_h, q_v and writes u+, p_h+, p_v+, q_h+, q_v+ (13 doubles)
+        rbytes = nf * W * H * 8 * 13 * 5 * 40
+        refine = {"ms_per_step": rms, "warps": 5, "iters": 40, "achieved_gbs": rbytes / (rms / 1e3) / 1e9,
+                  "note": "state 104 B/pixel is L2-resident; achieved is algorithmic bytes / time (can exceed HBM)"}
 
     # end to end through the public C ABI with host buffers
     e2e = None
@@ -376,6 +390,7 @@ def main():
                        "fps": world * nf / (ms / 1e3), "parallelism": f"frames x{world}",
                        "l2": "flushed between timed steps (256 MB write outside events); step working set ~1 GB"},
             "roofline": roofline,
+            "refine": refine,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,

@@ -147,7 +147,8 @@ DMM_API dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, con
  * prox Eq. pprox) on the two-slope convex approximation of the
  * data term around the current solution, re-approximated
  * `warps` times with `iters` iterations each (5 x 40 in P:497).
- * Weights w_h / w_v of the config; float32 on the device.  Readings
+ * Weights w_h / w_v of the config; float64 on the device (the oracle's precision;
+ * u_out is rounded to float32).  Readings
  * R24-R28: h in label units, linear interpolation of D between
  * labels, tau * sigma * 8 < 1 for convergence (0.35 / 0.35 suggested).
  * eps = 1, C = trunc gives the discrete model's truncated-linear r.
@@ -157,9 +158,9 @@ DMM_API dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, con
  * of one warp are captured once into a CUDA graph (per frame and parameters)
  * and replayed. */
 typedef struct dmm_refine_params {
-    float eps, delta, C;      /* penalty r: slope eps up to delta, slope 1, truncated at C  */
-    float h;                  /* data approximation step / trust region (labels)          */
-    float tau, sigma;         /* primal / dual step sizes                                   */
+    double eps, delta, C;     /* penalty r: slope eps up to delta, slope 1, truncated at C  */
+    double h;                 /* data approximation step / trust region (labels)          */
+    double tau, sigma;        /* primal / dual step sizes                                   */
     int32_t warps, iters;     /* re-approximations x PDHG iterations each                   */
 } dmm_refine_params;
 DMM_API dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* u_out, double* energy,

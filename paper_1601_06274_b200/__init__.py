@@ -50,9 +50,9 @@ class DmmConfig(ctypes.Structure):
 
 
 class DmmRefineParams(ctypes.Structure):
-    _fields_ = [("eps", ctypes.c_float), ("delta", ctypes.c_float), ("C", ctypes.c_float), ("h", ctypes.c_float),
-                ("tau", ctypes.c_float), ("sigma", ctypes.c_float), ("warps", ctypes.c_int32),
-                ("iters", ctypes.c_int32)]
+    _fields_ = [("eps", ctypes.c_double), ("delta", ctypes.c_double), ("C", ctypes.c_double),
+                ("h", ctypes.c_double), ("tau", ctypes.c_double), ("sigma", ctypes.c_double),
+                ("warps", ctypes.c_int32), ("iters", ctypes.c_int32)]
 
 
 class DmmXfer(ctypes.Structure):

@@ -303,8 +303,8 @@ dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
     DMM_DEVICE_GUARD(ctx);
     dmm_status st = frame_ok(ctx, frame);
     if (st || (st = not_sharded(ctx, "dmm_refine"))) return st;
-    if (!prm || prm->warps < 0 || prm->iters < 0 || prm->iters > 4096 || !(prm->h > 0.f) || !(prm->tau > 0.f) ||
-        !(prm->sigma > 0.f) || !(prm->eps >= 0.f && prm->eps <= 1.f) || !(prm->delta >= 0.f) || !(prm->C >= 0.f)) {
+    if (!prm || prm->warps < 0 || prm->iters < 0 || prm->iters > 4096 || !(prm->h > 0.0) || !(prm->tau > 0.0) ||
+        !(prm->sigma > 0.0) || !(prm->eps >= 0.0 && prm->eps <= 1.0) || !(prm->delta >= 0.0) || !(prm->C >= 0.0)) {
         ctx->err = "bad refinement parameters";
         return DMM_E_ARG;
     }

@@ -9,13 +9,15 @@
 //   (Eq. r-decompose); data prox P:431-440; warping P:441.
 // Readings R24-R28 as the oracle (oracle/refine.py).
 //
-// Per pixel state (float [H][W] each): u (two buffers), u0 (expansion point),
-// s1, s2 (slopes), p_h, p_v (duals of R_+), q_h, q_v (two buffers each; duals
-// of R_-), edge arrays indexed by the edge's first pixel.  An iteration is two
-// stencil kernels (primal: u, q; dual: p), one thread per pixel; the state
-// (44 B/pixel, 20 MB at C2) stays L2-resident across iterations.  A warp's
-// `iters` iterations (2*iters launches) are captured once into a CUDA graph
-// per (frame, parameters) and replayed.
+// Per pixel state (double [H][W] each): u, p_h, p_v, q_h, q_v (two buffers
+// each: every iteration reads one and writes the other, so no thread reads a
+// value another thread of the same launch updates), u0 (expansion point), s1,
+// s2 (slopes); edge arrays are indexed by the edge's first pixel.  An
+// iteration is ONE stencil kernel, one thread per pixel (the dual step's
+// neighbouring u+ are recomputed redundantly instead of a second launch); the
+// state (104 B/pixel, 48 MB at C2) stays L2-resident across iterations.  A
+// warp's `iters` iterations are captured once into a CUDA graph per (frame,
+// parameters) and replayed.
 #include <cmath>
 #include <cstring>
 
@@ -26,39 +28,41 @@ namespace dmm {
 namespace {
 
 constexpr int kRX = 32, kRY = 8;
-constexpr int kRefArrays = 11;   // u0buf, u1buf, u0(expansion), s1, s2, ph, pv, qh0, qv0, qh1, qv1
+// u (buffers 0, 1), u0 (expansion point), s1, s2, then per buffer b: ph, pv, qh, qv at 5 + 4b
+constexpr int kRefArrays = 13;
+using real = double;             // float64, the oracle's precision
 
 struct RefArgs {
-    float* rf;           // kRefArrays x [H][W]
+    real* rf;            // kRefArrays x [H][W]
     const uint8_t* D;    // [H][W][KP]
     const uint8_t* labels;
     int W, H, K, KP;
-    float wh, wv, eps, delta, C, h, tau, sigma;
+    real wh, wv, eps, delta, C, h, tau, sigma;
 };
 
-__device__ __forceinline__ float* arr(const RefArgs& a, int k) { return a.rf + (size_t)k * a.W * a.H; }
+__device__ __forceinline__ real* arr(const RefArgs& a, int k) { return a.rf + (size_t)k * a.W * a.H; }
 
 // D at a real label (reading R26): linear interpolation, label clamped to [0, K-1]
-__device__ __forceinline__ float d_interp(const uint8_t* Dp, int K, float u) {
-    const float uc = fminf(fmaxf(u, 0.f), (float)(K - 1));
-    const int k0 = min((int)floorf(uc), K - 1);
+__device__ __forceinline__ real d_interp(const uint8_t* Dp, int K, real u) {
+    const real uc = fmin(fmax(u, 0.0), (real)(K - 1));
+    const int k0 = min((int)floor(uc), K - 1);
     const int k1 = min(k0 + 1, K - 1);
-    const float f = uc - (float)k0;
-    return (1.f - f) * (float)Dp[k0] + f * (float)Dp[k1];
+    const real f = uc - (real)k0;
+    return (1.0 - f) * (real)Dp[k0] + f * (real)Dp[k1];
 }
 
 // prox of step * (w r_{a,b})^* (Eq. pprox)
-__device__ __forceinline__ float prox_conj(float t, float w, float a, float b, float step) {
-    const float aw = a * w, at = fabsf(t);
-    const float tp = at <= aw ? t : copysignf(fmaxf(aw, at - b * step), t);
-    return fminf(fmaxf(tp, -w), w);
+__device__ __forceinline__ real prox_conj(real t, real w, real a, real b, real step) {
+    const real aw = a * w, at = fabs(t);
+    const real tp = at <= aw ? t : copysign(fmax(aw, at - b * step), t);
+    return fmin(fmax(tp, -w), w);
 }
 
-__device__ __forceinline__ float r_dc(float t, float eps, float delta, float C) {
-    const float at = fabsf(t);
-    const float bp = C + delta - eps * delta;
-    const float rp = at <= delta ? eps * at : at - delta * (1.f - eps);
-    const float rm = at <= bp ? 0.f : at - bp;
+__device__ __forceinline__ real r_dc(real t, real eps, real delta, real C) {
+    const real at = fabs(t);
+    const real bp = C + delta - eps * delta;
+    const real rp = at <= delta ? eps * at : at - delta * (1.0 - eps);
+    const real rm = at <= bp ? 0.0 : at - bp;
     return rp - rm;
 }
 
@@ -66,8 +70,8 @@ __global__ void refine_init_kernel(RefArgs a) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const size_t i = (size_t)y * a.W + x;
-    arr(a, 0)[i] = (float)a.labels[i];
-    for (int k = 5; k < kRefArrays; ++k) arr(a, k)[i] = 0.f;
+    arr(a, 0)[i] = (real)a.labels[i];
+    for (int k = 5; k < kRefArrays; ++k) arr(a, k)[i] = 0.0;
 }
 
 // a new expansion point: u0 = u, two-slope approximation (R24)
@@ -75,90 +79,91 @@ __global__ void refine_warp_kernel(RefArgs a) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const size_t i = (size_t)y * a.W + x;
-    const float u0 = arr(a, 0)[i];
+    const real u0 = arr(a, 0)[i];
     const uint8_t* Dp = a.D + i * a.KP;
-    const float dc = d_interp(Dp, a.K, u0);
-    float s1 = (dc - d_interp(Dp, a.K, u0 - a.h)) / a.h;
-    float s2 = (d_interp(Dp, a.K, u0 + a.h) - dc) / a.h;
-    if (s2 < s1) { const float m = 0.5f * (s1 + s2); s1 = m; s2 = m; }
+    const real dc = d_interp(Dp, a.K, u0);
+    real s1 = (dc - d_interp(Dp, a.K, u0 - a.h)) / a.h;
+    real s2 = (d_interp(Dp, a.K, u0 + a.h) - dc) / a.h;
+    if (s2 < s1) { const real m = 0.5 * (s1 + s2); s1 = m; s2 = m; }
     arr(a, 2)[i] = u0;
     arr(a, 3)[i] = s1;
     arr(a, 4)[i] = s2;
 }
 
-// primal step: u+ (buffer 1 - cur) and q+ (q buffer 1 - cur) from u, p, q (buffer cur)
-__global__ void refine_primal_kernel(RefArgs a, int cur) {
-    const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
-    if (x >= a.W || y >= a.H) return;
+// u+ at pixel j = (jy, jx): prox_{tau D~}(u - tau A^T (p - q)) (R25)
+__device__ __forceinline__ real primal_u(const RefArgs& a, const real* u, const real* ph, const real* pv,
+                                         const real* qh, const real* qv, int jx, int jy) {
     const int W = a.W, H = a.H;
-    const size_t i = (size_t)y * W + x;
-    const float* u = arr(a, cur);
-    float* un = arr(a, 1 - cur);
-    const float* ph = arr(a, 5);
-    const float* pv = arr(a, 6);
-    const float* qh = arr(a, cur ? 9 : 7);
-    const float* qv = arr(a, cur ? 10 : 8);
-    float* qhn = arr(a, cur ? 7 : 9);
-    float* qvn = arr(a, cur ? 8 : 10);
-    // A^T (p - q) at pixel i
-    float div = 0.f;
-    if (x + 1 < W) div += ph[i] - qh[i];
-    if (x > 0) div -= ph[i - 1] - qh[i - 1];
-    if (y + 1 < H) div += pv[i] - qv[i];
-    if (y > 0) div -= pv[i - W] - qv[i - W];
-    const float ui = u[i];
-    const float uh = ui - a.tau * div;
-    // prox of tau D~ (reading R25)
-    const float u0 = arr(a, 2)[i], s1 = arr(a, 3)[i], s2 = arr(a, 4)[i];
-    float v = uh > u0 + a.tau * s2 ? uh - a.tau * s2 : (uh < u0 + a.tau * s1 ? uh - a.tau * s1 : u0);
-    un[i] = fminf(fmaxf(v, u0 - a.h), u0 + a.h);
-    // q+ = prox_{tau R_-^*}(q + tau A u) on the pixel's own (right, down) edges
-    const float bp = a.C + a.delta - a.eps * a.delta;
-    if (x + 1 < W) qhn[i] = prox_conj(qh[i] + a.tau * (ui - u[i + 1]), a.wh, 0.f, bp, a.tau);
-    if (y + 1 < H) qvn[i] = prox_conj(qv[i] + a.tau * (ui - u[i + W]), a.wv, 0.f, bp, a.tau);
+    const size_t j = (size_t)jy * W + jx;
+    real div = 0.0;
+    if (jx + 1 < W) div += ph[j] - qh[j];
+    if (jx > 0) div -= ph[j - 1] - qh[j - 1];
+    if (jy + 1 < H) div += pv[j] - qv[j];
+    if (jy > 0) div -= pv[j - W] - qv[j - W];
+    const real uh = u[j] - a.tau * div;
+    const real u0 = arr(a, 2)[j], s1 = arr(a, 3)[j], s2 = arr(a, 4)[j];
+    const real v = uh > u0 + a.tau * s2 ? uh - a.tau * s2 : (uh < u0 + a.tau * s1 ? uh - a.tau * s1 : u0);
+    return fmin(fmax(v, u0 - a.h), u0 + a.h);
 }
 
-// dual step: p+ = prox_{sigma R_+^*}(p + sigma A(2 u+ - u)) on the pixel's own edges
-__global__ void refine_dual_kernel(RefArgs a, int cur) {
+// One whole iteration (Eq. cont_iterates) in one kernel: the thread of pixel
+// i computes u+ at i and at its right / down neighbours (the dual step of the
+// pixel's own edges needs them: a 3-point redundant primal instead of a second
+// launch), then q+ (from u) and p+ (from 2u+ - u) of its own edges.  Reads
+// buffer cur, writes buffer 1 - cur (u, q) and p in place (each edge owned by
+// one pixel, read by no other thread of this launch).
+__global__ void refine_iter_kernel(RefArgs a, int cur) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const int W = a.W, H = a.H;
     const size_t i = (size_t)y * W + x;
-    const float* u = arr(a, cur);
-    const float* un = arr(a, 1 - cur);
-    const float bi = 2.f * un[i] - u[i];
+    const real* u = arr(a, cur);
+    real* un = arr(a, 1 - cur);
+    const int b0 = 5 + 4 * cur, b1 = 5 + 4 * (1 - cur);
+    const real* ph = arr(a, b0);
+    const real* pv = arr(a, b0 + 1);
+    const real* qh = arr(a, b0 + 2);
+    const real* qv = arr(a, b0 + 3);
+    const real ui = u[i];
+    const real uni = primal_u(a, u, ph, pv, qh, qv, x, y);
+    const real bp = a.C + a.delta - a.eps * a.delta;
+    const real bi = 2.0 * uni - ui;
     if (x + 1 < W) {
-        float* ph = arr(a, 5);
-        ph[i] = prox_conj(ph[i] + a.sigma * (bi - (2.f * un[i + 1] - u[i + 1])), a.wh, a.eps, a.delta, a.sigma);
+        const real unr = primal_u(a, u, ph, pv, qh, qv, x + 1, y);
+        const real ur = u[i + 1];
+        arr(a, b1 + 2)[i] = prox_conj(qh[i] + a.tau * (ui - ur), a.wh, 0.0, bp, a.tau);       // q+ = prox(q + tau A u)
+        arr(a, b1)[i] = prox_conj(ph[i] + a.sigma * (bi - (2.0 * unr - ur)), a.wh, a.eps, a.delta, a.sigma);
     }
     if (y + 1 < H) {
-        float* pv = arr(a, 6);
-        pv[i] = prox_conj(pv[i] + a.sigma * (bi - (2.f * un[i + W] - u[i + W])), a.wv, a.eps, a.delta, a.sigma);
+        const real und = primal_u(a, u, ph, pv, qh, qv, x, y + 1);
+        const real ud = u[i + W];
+        arr(a, b1 + 3)[i] = prox_conj(qv[i] + a.tau * (ui - ud), a.wv, 0.0, bp, a.tau);
+        arr(a, b1 + 1)[i] = prox_conj(pv[i] + a.sigma * (bi - (2.0 * und - ud)), a.wv, a.eps, a.delta, a.sigma);
     }
+    un[i] = uni;
 }
 
-__global__ void refine_swap_kernel(RefArgs a) {
+__global__ void refine_swap_kernel(RefArgs a) {     // odd iteration count: the state back to buffer 0
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
     const size_t i = (size_t)y * a.W + x;
     arr(a, 0)[i] = arr(a, 1)[i];
-    arr(a, 7)[i] = arr(a, 9)[i];
-    arr(a, 8)[i] = arr(a, 10)[i];
+    for (int k = 0; k < 4; ++k) arr(a, 5 + k)[i] = arr(a, 9 + k)[i];
 }
 
 // output (disparity units) and the energy E(u) = D(u) + R(Au), double accumulation
-__global__ void refine_out_kernel(RefArgs a, int cur, float d_min, float* out, double* energy) {
+__global__ void refine_out_kernel(RefArgs a, real d_min, float* out, double* energy) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     double e = 0.0;
     if (x < a.W && y < a.H) {
         const int W = a.W;
         const size_t i = (size_t)y * W + x;
-        const float* u = arr(a, cur);
-        const float ui = u[i];
-        if (out) out[i] = d_min + ui;
+        const real* u = arr(a, 0);
+        const real ui = u[i];
+        if (out) out[i] = (float)(d_min + ui);
         e = d_interp(a.D + i * a.KP, a.K, ui);
-        if (x + 1 < W) e += (double)a.wh * r_dc(ui - u[i + 1], a.eps, a.delta, a.C);
-        if (y + 1 < a.H) e += (double)a.wv * r_dc(ui - u[i + W], a.eps, a.delta, a.C);
+        if (x + 1 < W) e += a.wh * r_dc(ui - u[i + 1], a.eps, a.delta, a.C);
+        if (y + 1 < a.H) e += a.wv * r_dc(ui - u[i + W], a.eps, a.delta, a.C);
     }
     for (int d = 16; d > 0; d >>= 1) e += __shfl_down_sync(0xffffffffu, e, d);
     __shared__ double part[kRX * kRY / 32];
@@ -174,26 +179,26 @@ __global__ void refine_out_kernel(RefArgs a, int cur, float d_min, float* out, d
 
 }  // namespace
 
-size_t refine_bytes(int W, int H) { return (size_t)kRefArrays * 4 * W * H; }
+size_t refine_bytes(int W, int H) { return (size_t)kRefArrays * sizeof(real) * W * H; }
 
 dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,
                       cudaStream_t s) {
     FramePtrs P = frame_ptrs(ctx->L, frame);
     RefArgs a;
-    a.rf = P.rf;
+    a.rf = reinterpret_cast<real*>(P.rf);
     a.D = P.D;
     a.labels = P.labels;
     a.W = ctx->L.W; a.H = ctx->L.H; a.K = ctx->K; a.KP = ctx->KP;
-    a.wh = (float)ctx->cfg.w_h; a.wv = (float)ctx->cfg.w_v;
+    a.wh = (real)ctx->cfg.w_h; a.wv = (real)ctx->cfg.w_v;
     a.eps = prm->eps; a.delta = prm->delta; a.C = prm->C; a.h = prm->h; a.tau = prm->tau; a.sigma = prm->sigma;
     const dim3 grid((a.W + kRX - 1) / kRX, (a.H + kRY - 1) / kRY), blk(kRX, kRY);
     refine_init_kernel<<<grid, blk, 0, s>>>(a);
     ++ctx->launches;
-    // one warp = the expansion kernel + `iters` (primal, dual) pairs; an even
-    // number of iterations leaves u in buffer 0.  Captured once per
-    // (frame, parameters) into a graph on the context's capture stream.
+    // one warp = the expansion kernel + `iters` iteration kernels (+ a swap for
+    // an odd count, so the state ends in buffer 0).  Captured once per (frame,
+    // parameters) into a graph on the context's capture stream, replayed on `s`.
     RefineGraph& g = ctx->rg;
-    const bool same = g.exec && g.frame == frame && memcmp(&g.prm, prm, sizeof(*prm)) == 0 && g.rf == a.rf;
+    const bool same = g.exec && g.frame == frame && memcmp(&g.prm, prm, sizeof(*prm)) == 0 && g.rf == P.rf;
     if (!same) {
         if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
         if (!g.cap && cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking) != cudaSuccess)
@@ -204,11 +209,10 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
         refine_warp_kernel<<<grid, blk, 0, g.cap>>>(a);
         int cur = 0;
         for (int it = 0; it < prm->iters; ++it) {
-            refine_primal_kernel<<<grid, blk, 0, g.cap>>>(a, cur);
-            refine_dual_kernel<<<grid, blk, 0, g.cap>>>(a, cur);
+            refine_iter_kernel<<<grid, blk, 0, g.cap>>>(a, cur);
             cur ^= 1;
         }
-        if (cur) refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a);   // odd iters: the state back to buffers 0
+        if (cur) refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a);
         e = cudaStreamEndCapture(g.cap, &graph);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine capture end");
         e = cudaGraphInstantiate(&g.exec, graph, 0);
@@ -216,14 +220,14 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine graph instantiate");
         g.frame = frame;
         g.prm = *prm;
-        g.rf = a.rf;
+        g.rf = P.rf;
     }
     for (int w = 0; w < prm->warps; ++w) {
         cudaError_t e = cudaGraphLaunch(g.exec, s);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine graph launch");
-        ctx->launches += 1 + 2 * prm->iters + (prm->iters & 1);
+        ctx->launches += 1 + prm->iters + (prm->iters & 1);
     }
-    refine_out_kernel<<<grid, blk, 0, s>>>(a, 0, (float)ctx->cfg.d_min, out, energy_dev);
+    refine_out_kernel<<<grid, blk, 0, s>>>(a, (real)ctx->cfg.d_min, out, energy_dev);
     ++ctx->launches;
     return cuda_status(ctx, cudaGetLastError(), "refine");
 }
