@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(
             ["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-fopenmp", "-Wall", "-Wextra",
-             "-o", tmp, _SRC]
+             "-o", tmp, _SRC, "-lm"]
         )
         os.replace(tmp, _LIB)
     return _LIB
@@ -54,8 +54,18 @@ def _load():
         lib.oracle_dmm.argtypes = [P, i32, i32, i32, i32, i32, i32, i32, i32, P, P, P, P, P, i32]
         lib.oracle_energy.argtypes = [P, P, i32, i32, i32, i32, i32, i32]
         lib.oracle_energy.restype = i64
+        lib.oracle_edge_weights.argtypes = [P, i32, i32, P, P]
+        lib.oracle_dmm_general.argtypes = [P, i32, i32, i32, i32, i32, Pen, P, P, i32, i32, P, P, P, P, P, i32]
+        lib.oracle_energy_general.argtypes = [P, P, i32, i32, i32, i32, i32, Pen, P, P, i32]
+        lib.oracle_energy_general.restype = i64
+        lib.oracle_hm_general.argtypes = [P, i32, i32, i32, Pen, P, P]
         _lib = lib
     return _lib
+
+
+class Pen(ctypes.Structure):
+    """oracle_pen: R(d) = min(e1*min(d, delta) + e2*max(d - delta, 0), c) (units 2^-F)."""
+    _fields_ = [("e1", ctypes.c_int32), ("e2", ctypes.c_int32), ("delta", ctypes.c_int32), ("c", ctypes.c_int32)]
 
 
 def _p(a: np.ndarray | None):
@@ -161,3 +171,51 @@ def solve(left, right, d_min: int, K: int, w: int = 3, T: int = 4, Fbits: int = 
     out = dmm(D, w, w, T, Fbits, iters, nthreads)
     out.update(codes_left=cl, codes_right=cr, D=D)
     return out
+
+
+# ---------------------------------------------------- NEXT-3 general model
+def edge_weights(img):
+    """Quantised edge-aware weights (om_h, om_v) in [1, 16] (reading R30)."""
+    img = _c(img, np.uint8)
+    H, W = img.shape
+    oh = np.zeros((H, W), np.uint8)
+    ov = np.zeros((H, W), np.uint8)
+    _load().oracle_edge_weights(_p(img), W, H, _p(oh), _p(ov))
+    return oh, ov
+
+
+def hm_general(F, w: int, pen, om=None) -> np.ndarray:
+    F = _c(F, np.int64)
+    n, K = F.shape
+    lam = np.zeros_like(F)
+    omc = None if om is None else _c(om, np.uint8)
+    _load().oracle_hm_general(_p(F), n, K, w, Pen(*pen), _p(omc), _p(lam))
+    return lam
+
+
+def dmm_general(D, w_h: int, w_v: int, pen, Fbits: int, iters: int, om_h=None, om_v=None, nthreads: int = 1):
+    """Dual MM with the general penalty pen = (e1, e2, delta, c) and optional
+    edge weights; returns dict(fdual, gdual, labels, bound_hist, energy)."""
+    D = _c(D, np.uint8)
+    H, W, K = D.shape
+    f = np.zeros((H, W, K), np.int64)
+    g = np.zeros((H, W, K), np.int64)
+    lab = np.zeros((H, W), np.int32)
+    bh = np.zeros(2 * max(iters, 1), np.int64)
+    e = np.zeros(1, np.int64)
+    oh = None if om_h is None else _c(om_h, np.uint8)
+    ov = None if om_v is None else _c(om_v, np.uint8)
+    rc = _load().oracle_dmm_general(_p(D), W, H, K, w_h, w_v, Pen(*pen), _p(oh), _p(ov), Fbits, iters, _p(f), _p(g),
+                                    _p(lab), _p(bh), _p(e), nthreads)
+    if rc:
+        raise ValueError("oracle_dmm_general: bad arguments")
+    return dict(fdual=f, gdual=g, labels=lab, bound_hist=bh, energy=int(e[0]))
+
+
+def energy_general(D, labels, w_h: int, w_v: int, pen, Fbits: int, om_h=None, om_v=None) -> int:
+    D = _c(D, np.uint8)
+    labels = _c(labels, np.int32)
+    H, W, K = D.shape
+    oh = None if om_h is None else _c(om_h, np.uint8)
+    ov = None if om_v is None else _c(om_v, np.uint8)
+    return int(_load().oracle_energy_general(_p(D), _p(labels), W, H, K, w_h, w_v, Pen(*pen), _p(oh), _p(ov), Fbits))

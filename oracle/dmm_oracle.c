@@ -335,3 +335,190 @@ int oracle_dmm(const uint8_t* D, int W, int H, int K, int w_h, int w_v, int T,
     free(f); free(g); free(lab);
     return 0;
 }
+
+
+/* =========================================================================
+ * NEXT-3: general penalty + edge weights.  A separate, literal implementation
+ * (direct enumeration of every Msg, three Msg per Handshake as Alg.5 prints
+ * it) so that the classic path above stays exactly as pinned.
+ * ========================================================================= */
+#include <math.h>
+
+static int64_t gen_R(const oracle_pen* p, int64_t d) {
+    if (d < 0) d = -d;
+    const int64_t lin = (int64_t)p->e1 * (d < p->delta ? d : p->delta) +
+                        (int64_t)p->e2 * (d > p->delta ? d - p->delta : 0);
+    return lin < p->c ? lin : p->c;
+}
+
+/* V_ij(d) = floor(w * om * R(|d|) / 16) */
+static int64_t gen_V(const oracle_pen* p, int64_t w, int om, int64_t d) {
+    return (w * (int64_t)om * gen_R(p, d)) / 16;
+}
+
+void oracle_edge_weights(const uint8_t* img, int W, int H, uint8_t* om_h, uint8_t* om_v) {
+    uint8_t lut[256];
+    for (int g = 0; g < 256; ++g) {
+        double v = floor(16.0 * exp(-5.0 * (double)g / 255.0) + 0.5);
+        lut[g] = (uint8_t)(v < 1.0 ? 1 : (v > 16.0 ? 16 : v));
+    }
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            const int i = img[(size_t)y * W + x];
+            om_h[(size_t)y * W + x] = x + 1 < W ? lut[abs(i - img[(size_t)y * W + x + 1])] : 16;
+            om_v[(size_t)y * W + x] = y + 1 < H ? lut[abs(i - img[(size_t)(y + 1) * W + x])] : 16;
+        }
+}
+
+/* Msg over one edge (Eq. msg-pass) by enumeration. */
+static void gen_msg(const int64_t* a, int K, const oracle_pen* p, int64_t w, int om, int64_t* out) {
+    for (int b = 0; b < K; ++b) {
+        int64_t best = a[0] + gen_V(p, w, om, b);
+        for (int x = 1; x < K; ++x) best = min64(best, a[x] + gen_V(p, w, om, x - b));
+        out[b] = best;
+    }
+}
+
+typedef struct {
+    const int64_t* F; int K; int64_t w; const oracle_pen* p; const uint8_t* om; int64_t* lam;
+} hmg_job;
+
+static int gen_om(const hmg_job* J, int e) { return J->om ? J->om[e] : 16; }
+
+/* hm_rec of the general model (same recursion, readings R5/R7/R8/R9/R10);
+ * edge e joins nodes e and e+1. */
+static void hmg_rec(const hmg_job* J, int lo, int hi, const int64_t* L, const int64_t* R) {
+    const int K = J->K;
+    if (lo == hi) {
+        for (int k = 0; k < K; ++k) J->lam[(size_t)lo * K + k] = L[k] + J->F[(size_t)lo * K + k] + R[k];
+        return;
+    }
+    int len = hi - lo + 1;
+    int i = lo + len / 2 - 1, j = i + 1;
+    int64_t* buf = (int64_t*)malloc((size_t)7 * K * sizeof(int64_t));
+    int64_t *phiL = buf, *phiR = buf + K, *tmp = buf + 2 * K, *phi_ji = buf + 3 * K;
+    int64_t *m = buf + 4 * K, *phi_ij = buf + 5 * K, *phi_ji2 = buf + 6 * K;
+    memcpy(phiL, L, (size_t)K * sizeof(int64_t));
+    for (int p = lo; p < i; ++p) {                 /* into p+1 over edge p */
+        vadd(tmp, phiL, &J->F[(size_t)p * K], K);
+        gen_msg(tmp, K, J->p, J->w, gen_om(J, p), phiL);
+    }
+    memcpy(phiR, R, (size_t)K * sizeof(int64_t));
+    for (int p = hi; p > j; --p) {                 /* into p-1 over edge p-1 */
+        vadd(tmp, phiR, &J->F[(size_t)p * K], K);
+        gen_msg(tmp, K, J->p, J->w, gen_om(J, p - 1), phiR);
+    }
+    const int om = gen_om(J, i);                   /* the Handshake edge ij */
+    vadd(tmp, &J->F[(size_t)j * K], phiR, K);
+    gen_msg(tmp, K, J->p, J->w, om, phi_ji);                          /* Alg.5 line 1 */
+    for (int k = 0; k < K; ++k) m[k] = phiL[k] + J->F[(size_t)i * K + k] + phi_ji[k];   /* line 2 */
+    for (int k = 0; k < K; ++k) tmp[k] = floor_half(m[k] - 2 * phi_ji[k]);
+    gen_msg(tmp, K, J->p, J->w, om, phi_ij);                          /* line 3 (R9) */
+    for (int k = 0; k < K; ++k) tmp[k] = -phi_ij[k];
+    gen_msg(tmp, K, J->p, J->w, om, phi_ji2);                         /* line 4: bounce back */
+    hmg_rec(J, lo, i, L, phi_ji2);
+    hmg_rec(J, j, hi, phi_ij, R);
+    free(buf);
+}
+
+void oracle_hm_general(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int64_t* lam) {
+    if (n < 1 || K < 1) return;
+    hmg_job J = {F, K, w, &pen, om, lam};
+    int64_t* zero = (int64_t*)calloc((size_t)K, sizeof(int64_t));
+    hmg_rec(&J, 0, n - 1, zero, zero);
+    free(zero);
+}
+
+int64_t oracle_energy_general(const uint8_t* D, const int32_t* labels, int W, int H, int K, int w_h, int w_v,
+                              oracle_pen pen, const uint8_t* om_h, const uint8_t* om_v, int Fbits) {
+    int64_t e = 0;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            const size_t q = (size_t)y * W + x;
+            const int32_t l = labels[q];
+            e += (int64_t)D[q * K + l] << Fbits;
+            if (x + 1 < W) e += gen_V(&pen, w_h, om_h ? om_h[q] : 16, l - labels[q + 1]);
+            if (y + 1 < H) e += gen_V(&pen, w_v, om_v ? om_v[q] : 16, l - labels[q + W]);
+        }
+    return e;
+}
+
+/* Algorithm 2 as oracle_dmm, with the general chains. */
+int oracle_dmm_general(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
+                       const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int64_t* fdual,
+                       int64_t* gdual, int32_t* labels, int64_t* bound_hist, int64_t* energy, int nthreads) {
+    if (!D || W < 1 || H < 1 || K < 1 || K > 256 || w_h < 0 || w_v < 0 || pen.e1 < 0 || pen.e2 < pen.e1 ||
+        pen.delta < 0 || pen.c < 0 || Fbits < 0 || Fbits > 16 || iters < 1)
+        return 1;
+    const size_t N = (size_t)W * H * K;
+    const int64_t scale = (int64_t)1 << Fbits;
+    int64_t* f = (int64_t*)calloc(N, sizeof(int64_t));
+    int64_t* g = (int64_t*)calloc(N, sizeof(int64_t));
+    int32_t* lab = (int32_t*)malloc((size_t)W * H * sizeof(int32_t));
+#ifdef _OPENMP
+    int nth = nthreads > 1 ? nthreads : 1;
+#endif
+    (void)nthreads;
+    for (int t = 0; t < iters; ++t) {
+        const int last = (t == iters - 1);
+        int64_t bh = 0, bv = 0;
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nth) reduction(+ : bh) schedule(dynamic, 1)
+#endif
+        for (int y = 0; y < H; ++y) {
+            int64_t* Fr = (int64_t*)malloc((size_t)W * K * sizeof(int64_t));
+            int64_t* h = (int64_t*)malloc((size_t)W * K * sizeof(int64_t));
+            uint8_t* om = (uint8_t*)malloc((size_t)W);
+            for (int x = 0; x < W; ++x) {
+                om[x] = om_h ? om_h[(size_t)y * W + x] : 16;
+                for (int k = 0; k < K; ++k) {
+                    size_t q = ((size_t)y * W + x) * K + k;
+                    Fr[(size_t)x * K + k] = (int64_t)D[q] * scale + g[q];
+                }
+            }
+            oracle_hm_general(Fr, W, K, w_h, pen, om, h);
+            for (int x = 0; x < W; ++x) {
+                int64_t mn = h[(size_t)x * K];
+                for (int k = 0; k < K; ++k) {
+                    size_t q = ((size_t)y * W + x) * K + k;
+                    f[q] = h[(size_t)x * K + k] - g[q];
+                    mn = min64(mn, h[(size_t)x * K + k]);
+                }
+                bh += mn;
+            }
+            free(Fr); free(h); free(om);
+        }
+#ifdef _OPENMP
+#pragma omp parallel for num_threads(nth) reduction(+ : bv) schedule(dynamic, 1)
+#endif
+        for (int x = 0; x < W; ++x) {
+            int64_t* Gc = (int64_t*)malloc((size_t)H * K * sizeof(int64_t));
+            int64_t* v = (int64_t*)malloc((size_t)H * K * sizeof(int64_t));
+            uint8_t* om = (uint8_t*)malloc((size_t)H);
+            for (int y = 0; y < H; ++y) {
+                om[y] = om_v ? om_v[(size_t)y * W + x] : 16;
+                for (int k = 0; k < K; ++k) Gc[(size_t)y * K + k] = f[((size_t)y * W + x) * K + k];
+            }
+            oracle_hm_general(Gc, H, K, w_v, pen, om, v);
+            for (int y = 0; y < H; ++y) {
+                int64_t mn = v[(size_t)y * K];
+                int32_t arg = 0;
+                for (int k = 0; k < K; ++k) {
+                    size_t q = ((size_t)y * W + x) * K + k;
+                    g[q] = v[(size_t)y * K + k] - f[q];
+                    if (v[(size_t)y * K + k] < mn) { mn = v[(size_t)y * K + k]; arg = k; }
+                }
+                bv += mn;
+                if (last) lab[(size_t)y * W + x] = arg;
+            }
+            free(Gc); free(v); free(om);
+        }
+        if (bound_hist) { bound_hist[2 * t] = bh; bound_hist[2 * t + 1] = bv; }
+    }
+    if (fdual) memcpy(fdual, f, N * sizeof(int64_t));
+    if (gdual) memcpy(gdual, g, N * sizeof(int64_t));
+    if (labels) memcpy(labels, lab, (size_t)W * H * sizeof(int32_t));
+    if (energy) *energy = oracle_energy_general(D, lab, W, H, K, w_h, w_v, pen, om_h, om_v, Fbits);
+    free(f); free(g); free(lab);
+    return 0;
+}

@@ -93,6 +93,36 @@ int oracle_dmm(const uint8_t* D, int W, int H, int K, int w_h, int w_v, int T,
 int64_t oracle_energy(const uint8_t* D, const int32_t* labels, int W, int H, int K,
                       int w_h, int w_v, int T);
 
+/* ---- NEXT-3: general penalty and edge weights (Fig.2; Eq.
+ * regularizer-form P:134-136; r-decompose P:364-375), readings R29-R31.
+ * R(d) = min(e1*min(d, delta) + e2*max(d - delta, 0), c)   (integers, units 2^-F:
+ *   slope e1 = eps*2^F up to delta, slope e2 = 2^F beyond, truncated at c = C*2^F),
+ * edge (i,j) of direction w (w_h / w_v) with quantised weight om in [1, 16]:
+ *   V_ij(d) = floor(w * om * R(|d|) / 16)   (om = 16: constant weights).
+ * With e1 = e2 = 2^F, c = T*2^F and om = 16 this is w*min(|d|,T)*2^F. */
+typedef struct { int32_t e1, e2, delta, c; } oracle_pen;
+
+/* Edge-aware weights (SPEC S:99 formula, quantised, reading R30):
+ * om(g) = clamp(round(16 exp(-5 g / 255)), 1, 16), g = |I_i - I_j| (u8).
+ * om_h[y][x]: edge (y,x)-(y,x+1); om_v[y][x]: edge (y,x)-(y+1,x); the last
+ * column / row entries are 16 (unused). */
+void oracle_edge_weights(const uint8_t* img, int W, int H, uint8_t* om_h, uint8_t* om_v);
+
+/* Dual MM (Algorithm 2) with the general pairwise term above: the same
+ * algorithm as oracle_dmm with every Msg = min_a a(a) + V_ij(|a-b|) by
+ * direct enumeration over the edge's own V (Alg.5 literal, three Msg per
+ * Handshake).  om_h / om_v nullable (= all 16).  Outputs as oracle_dmm;
+ * energy = D*2^F + sum V (already scaled).  Returns 0 / 1 (bad args). */
+int oracle_dmm_general(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
+                       const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int64_t* fdual,
+                       int64_t* gdual, int32_t* labels, int64_t* bound_hist, int64_t* energy, int nthreads);
+/* Energy of a labelling under the general model (scaled by 2^F). */
+int64_t oracle_energy_general(const uint8_t* D, const int32_t* labels, int W, int H, int K, int w_h, int w_v,
+                              oracle_pen pen, const uint8_t* om_h, const uint8_t* om_v, int Fbits);
+/* Hierarchical minorant of one chain under the general model: om[n-1] edge
+ * weights (nullable = 16), w the direction weight. */
+void oracle_hm_general(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int64_t* lam);
+
 #ifdef __cplusplus
 }
 #endif
