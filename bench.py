@@ -202,6 +202,10 @@ def main():
                          "step sharded over the GPUs, each GPU solving its frames as one batch (throughput mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pen", default=None,
+                    help="NEXT-3 general penalty e1,e2,delta,c (units 2^-F, e.g. 8,16,2,80: eps=1/2, delta=2, C=5) "
+                         "solved by the general int32 kernels")
+    ap.add_argument("--edge-weights", action="store_true", help="NEXT-3 edge-aware pairwise weights")
     ap.add_argument("--refine", action="store_true",
                     help="append the continuous refinement (NEXT-2: 5 warps x 40 PDHG iterations, P:497) to every "
                          "step (frames mode, one frame per GPU)")
@@ -236,8 +240,9 @@ def main():
     nf = (total_frames + world - 1) // world
     distinct = [datagen.pair(c["kind"], W, H, K, seed=rank * nf + s) for s in range(min(nf, 8))]
     left, right = distinct[0][0], distinct[0][1]
+    pen = tuple(int(v) for v in args.pen.split(",")) if args.pen else None
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
-                      max_iters=iters, batch=nf, device=dev)
+                      max_iters=iters, batch=nf, device=dev, pen=pen, edge_weights=args.edge_weights)
     Lh = np.stack([distinct[s % len(distinct)][0] for s in range(nf)])
     Rh = np.stack([distinct[s % len(distinct)][1] for s in range(nf)])
     lt = torch.from_numpy(Lh).to(dev)
@@ -387,6 +392,9 @@ def main():
                                       f"{total_frames} frames per step ({nf} per GPU, solved as one batch)"),
                        "W": W, "H": H, "K": K, "iters": iters, "w": W_REG, "T": T_REG, "frac_bits": FBITS,
                        "frames_per_gpu": nf,
+                       "pairwise": ("general penalty e1,e2,delta,c=" + args.pen if args.pen else
+                                    f"truncated linear w={W_REG}, T={T_REG}")
+                                   + (", edge-aware weights" if args.edge_weights else ""),
                        "fps": world * nf / (ms / 1e3), "parallelism": f"frames x{world}",
                        "l2": "flushed between timed steps (256 MB write outside events); step working set ~1 GB"},
             "roofline": roofline,

@@ -66,6 +66,20 @@ typedef struct dmm_config {
     int32_t oob_cost;        /* cost when x - d leaves the image; -1 => ((2r+1)^2-1)/2   */
     int32_t batch;           /* frames held by the context, >= 1 (C5 throughput mode)    */
     int32_t max_iters;       /* capacity of the per-frame bound history, >= 1            */
+    /* General pairwise model (NEXT-3; all zero = the truncated-linear model
+     * w * min(|a-b|, trunc) above).  Penalty in units of 2^-frac_bits:
+     *   R(d) = min(pen_e1*min(d, pen_delta) + pen_e2*max(d - pen_delta, 0), pen_c)
+     * (Fig.2 P:132-142 sampled at integer differences: slope eps = pen_e1/2^F
+     * up to delta, slope pen_e2/2^F beyond, truncated at C = pen_c/2^F;
+     * 0 <= pen_e1 <= pen_e2), and edge (i,j) of direction w (w_h / w_v) costs
+     *   V_ij(d) = floor(w * om_ij * R(|d|) / 16),
+     * om_ij = 16 (edge_weights = 0) or the edge-aware weight of the left image
+     * (edge_weights = 1): om = clamp(round(16 exp(-5 |I_i - I_j| / 255)), 1, 16)
+     * (Eq. regularizer-form; formula SPEC S:99, reading R30).
+     * trunc is not used in this mode.  Runs the int32 general kernels (hmg.cu);
+     * ROWCOL sharding is not available for it. */
+    int32_t pen_e1, pen_e2, pen_delta, pen_c;
+    int32_t edge_weights;
 } dmm_config;
 
 typedef struct dmm_ctx dmm_ctx;

@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary declared in include/dmm.h: argument
 // checks, workspace carving, kernel orchestration of Algorithm 2,
 // and error reporting.  No torch types cross this boundary.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -20,6 +21,9 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 bool valid(const dmm_config* c) {
     if (!c) return false;
+    if (c->pen_e1 < 0 || c->pen_e2 < c->pen_e1 || c->pen_delta < 0 || c->pen_c < 0 || c->pen_c > (1 << 20) ||
+        c->pen_e2 > (1 << 20) || (c->edge_weights != 0 && c->edge_weights != 1))
+        return false;
     const int K = c->d_max - c->d_min + 1;
     // width <= 16384: cost_kernel stages the row's two code rows (8 * W bytes) in
     // shared memory; W * H <= 2^28 keeps every pixel index in int32.
@@ -92,6 +96,12 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->flag = (int32_t*)take(8);
     off->rf = (float*)take(dmm::refine_bytes((int)W, (int)H));
     off->renergy = (double*)take(8);
+    if (dmm::gen_mode(c)) {
+        off->gfv = (int32_t*)take(4 * cells);
+        off->ggh = (int32_t*)take(4 * cells);
+        off->gom_h = (uint8_t*)take(px);
+        off->gom_v = (uint8_t*)take(px + 256);
+    }
     return o;
 }
 
@@ -175,6 +185,11 @@ dmm_status launch_half_on(dmm_ctx* ctx, const Layout& L, int frame, int nframes,
     a.bound_slot = 2 * t + v;
     a.nseg = nseg;
     a.segx = segx;
+    if (gen_mode(&ctx->cfg)) {
+        Timed tm(ctx, 2 + v, s, 0);
+        gen_half(ctx, frame, nframes, t, v, iterations, s);
+        return check_launch(ctx, "general half step");
+    }
     if (ctx->use_pair && ctx->pair_ok) {
         Timed tm(ctx, 2 + v, s, hm2_launches_per_pass(a, v));
         launch_hm2_pass(a, v, nframes, s);
@@ -214,7 +229,18 @@ size_t dmm_workspace_bytes(const dmm_config* cfg) {
 dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int device,
                       dmm_ctx** out) {
     if (!out || !valid(cfg) || !workspace || ((uintptr_t)workspace & 255)) return DMM_E_ARG;
-    if (span_bound(cfg) > 65535) return DMM_E_RANGE;
+    if (dmm::gen_mode(cfg)) {
+        // every message / minorant value is bounded by a chain's cost of the
+        // optimal labelling plus the same of the other orientation's dual;
+        // 4 n (maxD 2^F + 2 w c) < 2^30 keeps all int32 sums exact
+        const int bits = (2 * cfg->census_radius + 1) * (2 * cfg->census_radius + 1) - 1;
+        const long long maxD = (cfg->oob_cost > bits ? cfg->oob_cost : bits) << cfg->frac_bits;
+        const long long w = cfg->w_h > cfg->w_v ? cfg->w_h : cfg->w_v;
+        const long long n = cfg->width > cfg->height ? cfg->width : cfg->height;
+        if (4 * n * (maxD + 2 * w * cfg->pen_c) >= (1ll << 30)) return DMM_E_RANGE;
+    } else if (span_bound(cfg) > 65535) {
+        return DMM_E_RANGE;
+    }
     *out = nullptr;
     if (bytes < dmm_workspace_bytes(cfg)) return DMM_E_ARG;
     dmm_ctx* c = new (std::nothrow) dmm_ctx();
@@ -245,6 +271,10 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.flag = (int32_t*)(b + (size_t)off.flag);
     c->L.base.rf = (float*)(b + (size_t)off.rf);
     c->L.base.renergy = (double*)(b + (size_t)off.renergy);
+    c->L.base.gfv = (int32_t*)(b + (size_t)off.gfv);
+    c->L.base.ggh = (int32_t*)(b + (size_t)off.ggh);
+    c->L.base.gom_h = (uint8_t*)(b + (size_t)off.gom_h);
+    c->L.base.gom_v = (uint8_t*)(b + (size_t)off.gom_v);
     c->L.W = cfg->width; c->L.H = cfg->height; c->L.K = c->K; c->L.KP = c->KP;
     c->ws = b;
     c->ws_bytes = bytes;
@@ -253,12 +283,35 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->launches = 0;
     c->profiling = 0;
     c->stop_after_h = 0;
-    c->pair_ok = pair_range_ok(cfg);
+    c->pair_ok = dmm::gen_mode(cfg) ? 0 : pair_range_ok(cfg);
     c->use_pair = 1;
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         dmm_destroy(c);
         return DMM_E_CUDA;
+    }
+    if (dmm::gen_mode(cfg)) {
+        // edge-weight table (reading R30), computed on the host in double as
+        // the oracle does, uploaded after every frame's vertical weight map
+        uint8_t lut[256];
+        for (int g = 0; g < 256; ++g) {
+            const double v = floor(16.0 * exp(-5.0 * (double)g / 255.0) + 0.5);
+            lut[g] = (uint8_t)(v < 1.0 ? 1 : (v > 16.0 ? 16 : v));
+        }
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaError_t e = cudaSuccess;
+        for (int f = 0; f < cfg->batch && e == cudaSuccess; ++f) {
+            dmm::FramePtrs P = dmm::frame_ptrs(c->L, f);
+            e = cudaMemcpy(P.gom_v + (size_t)cfg->width * cfg->height, lut, 256, cudaMemcpyHostToDevice);
+            if (e == cudaSuccess && !cfg->edge_weights) {   // constant weights: the maps stay 16
+                e = cudaMemset(P.gom_h, 16, (size_t)cfg->width * cfg->height);
+                if (e == cudaSuccess) e = cudaMemset(P.gom_v, 16, (size_t)cfg->width * cfg->height);
+            }
+        }
+        if (prev >= 0) cudaSetDevice(prev);
+        if (e != cudaSuccess) { dmm_destroy(c); return DMM_E_CUDA; }
     }
     *out = c;
     return DMM_OK;
@@ -290,6 +343,7 @@ dmm_status dmm_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const u
     } else {
         { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, 1, ctx->cfg.census_radius, pitch, left, right, s); }
         { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, 1, ctx->cfg.d_min, ctx->oob, s); }
+        if (ctx->cfg.edge_weights) dmm::gen_weights(ctx, frame, left, pitch, s);
     }
     if ((st = check_launch(ctx, "cost_volume"))) return st;
     ctx->has_cost[frame] = 1;
@@ -384,9 +438,12 @@ dmm_status dmm_solve(dmm_ctx* ctx, int frame, int nframes, int32_t iterations, v
         return DMM_OK;
     }
     {
-        Timed tm(ctx, 4, s);
-        dmm::launch_energy(ctx->L, frame, nframes, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc,
-                           ctx->cfg.frac_bits, nullptr, nullptr, s);
+        Timed tm(ctx, 4, s, dmm::gen_mode(&ctx->cfg) ? 0 : 1);
+        if (dmm::gen_mode(&ctx->cfg))
+            dmm::gen_energy(ctx, frame, nframes, nullptr, nullptr, s);
+        else
+            dmm::launch_energy(ctx->L, frame, nframes, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc,
+                               ctx->cfg.frac_bits, nullptr, nullptr, s);
     }
     if ((st = check_launch(ctx, "solve"))) return st;
     for (int f = frame; f < frame + nframes; ++f) ctx->iters_done[f] = iterations;
@@ -473,8 +530,12 @@ dmm_status dmm_copy_dual(dmm_ctx* ctx, int frame, int which, int32_t* dst, void*
     if (!dst || (which != 0 && which != 1)) return DMM_E_ARG;
     if (ctx->iters_done[frame] == 0 || (ctx->iters_done[frame] == kPartial && which != 0)) return DMM_E_STATE;
     dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
-    dmm::launch_decode_rec(which ? P.fh : P.fv, which ? P.D : nullptr, ctx->cfg.frac_bits, dst,
-                           (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
+    if (dmm::gen_mode(&ctx->cfg))
+        dmm::launch_decode_dense(which ? P.ggh : P.gfv, which ? P.D : nullptr, ctx->cfg.frac_bits, dst,
+                                 (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
+    else
+        dmm::launch_decode_rec(which ? P.fh : P.fv, which ? P.D : nullptr, ctx->cfg.frac_bits, dst,
+                               (long long)ctx->L.W * ctx->L.H, ctx->K, ctx->KP, (cudaStream_t)stream);
     return check_launch(ctx, "copy dual");
 }
 
@@ -513,6 +574,8 @@ dmm_status dmm_cost_volume_frames(dmm_ctx* ctx, int frame, int nframes, const ui
     cudaStream_t s = (cudaStream_t)stream;
     { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, nframes, ctx->cfg.census_radius, pitch, left, right, s); }
     { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, nframes, ctx->cfg.d_min, ctx->oob, s); }
+    if (ctx->cfg.edge_weights)
+        for (int f = 0; f < nframes; ++f) dmm::gen_weights(ctx, frame + f, left + (size_t)f * pitch * ctx->L.H, pitch, s);
     if ((st = check_launch(ctx, "cost_volume_frames"))) return st;
     for (int f = frame; f < frame + nframes; ++f) { ctx->has_cost[f] = 1; ctx->iters_done[f] = 0; }
     return DMM_OK;
@@ -539,6 +602,8 @@ dmm_status dmm_run_host_frames(dmm_ctx* ctx, int frame, int nframes, const uint8
         return st;
     { Timed t(ctx, 0, s); dmm::launch_census(ctx->L, frame, nframes, ctx->cfg.census_radius, ctx->L.W, nullptr, nullptr, s); }
     { Timed t(ctx, 1, s); dmm::launch_cost(ctx->L, frame, nframes, ctx->cfg.d_min, ctx->oob, s); }
+    if (ctx->cfg.edge_weights)
+        for (int f = frame; f < frame + nframes; ++f) dmm::gen_weights(ctx, f, dmm::frame_ptrs(ctx->L, f).img_l, ctx->L.W, s);
     if ((st = check_launch(ctx, "run_host_frames"))) return st;
     for (int f = frame; f < frame + nframes; ++f) { ctx->has_cost[f] = 1; ctx->iters_done[f] = 0; }
     if ((st = dmm_solve(ctx, frame, nframes, iterations, stream))) return st;
@@ -650,8 +715,12 @@ dmm_status dmm_energy_of(dmm_ctx* ctx, int frame, const uint8_t* labels, int64_t
     if ((st = cuda_err(ctx, cudaMemsetAsync(bad, 0, 4, s), "memset flag"))) return st;
     {
         Timed tm(ctx, 4, s);
-        dmm::launch_energy(ctx->L, frame, 1, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc, ctx->cfg.frac_bits, labels,
-                           bad, s);
+        if (dmm::gen_mode(&ctx->cfg)) {
+            dmm::gen_energy(ctx, frame, 1, labels, bad, s);
+        } else {
+            dmm::launch_energy(ctx->L, frame, 1, ctx->cfg.w_h, ctx->cfg.w_v, ctx->cfg.trunc, ctx->cfg.frac_bits,
+                               labels, bad, s);
+        }
     }
     if ((st = check_launch(ctx, "energy"))) return st;
     if ((st = cuda_err(ctx, cudaMemcpyAsync(&e, P.energy, 8, cudaMemcpyDeviceToHost, s), "d2h"))) return st;

@@ -73,6 +73,12 @@ dmm_status shard_cost_volume(dmm_ctx* ctx, const uint8_t* left, const uint8_t* r
 dmm_status shard_solve(dmm_ctx* ctx, int iterations, cudaStream_t s);
 dmm_status shard_half_step(dmm_ctx* ctx, int t, int vertical, int iterations, cudaStream_t s);
 void shard_release(dmm_ctx* ctx);
+// hmg.cu (general pairwise model, NEXT-3)
+bool gen_mode(const dmm_config* c);
+int genR_host(const dmm_config& c, int d);
+void gen_weights(dmm_ctx* ctx, int frame, const uint8_t* left, int64_t pitch, cudaStream_t s);
+void gen_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations, cudaStream_t s);
+void gen_energy(dmm_ctx* ctx, int frame, int nframes, const uint8_t* labels, int32_t* bad, cudaStream_t s);
 // refine.cu
 size_t refine_bytes(int W, int H);
 dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,

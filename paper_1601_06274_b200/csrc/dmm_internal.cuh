@@ -44,8 +44,13 @@ struct FramePtrs {
     long long* bounds;   // [2 * max_iters]
     long long* energy;   // [1]
     int32_t* flag;       // [1] scratch: label-range flag of dmm_energy_of
-    float* rf;           // continuous refinement state (refine.cu): 11 x float [H][W]
+    float* rf;           // continuous refinement state (refine.cu)
     double* renergy;     // [1] energy of the refined labelling
+    // general pairwise model (hmg.cu; only allocated when the config asks for it)
+    int32_t* gfv;        // f_            int32 [H][W][KP]
+    int32_t* ggh;        // D*2^F + g_    int32 [H][W][KP]
+    uint8_t* gom_h;      // edge weights of horizontal edges [H][W]
+    uint8_t* gom_v;      // edge weights of vertical edges [H][W], then the 256-entry weight table
 };
 
 // Per-frame pointers are base + frame * stride (bytes).
@@ -76,6 +81,10 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.flag = (int32_t*)((char*)p.flag + o);
     p.rf = (float*)((char*)p.rf + o);
     p.renergy = (double*)((char*)p.renergy + o);
+    p.gfv = (int32_t*)((char*)p.gfv + o);
+    p.ggh = (int32_t*)((char*)p.ggh + o);
+    p.gom_h += o;
+    p.gom_v += o;
     return p;
 }
 
@@ -129,6 +138,9 @@ void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, i
 void launch_pad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);
 // Expand compact records to dense int32 [cells][K]; if D != nullptr subtract
 // D*2^fbits (recovers g_ from fh).
+// Dense int32 [cells][KP] duals (general model) -> dense [cells][K], minus D*2^F if D.
+void launch_decode_dense(const int32_t* src, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K, int KP,
+                         cudaStream_t s);
 void launch_decode_rec(const uint8_t* rec, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K,
                        int KP, cudaStream_t s);
 

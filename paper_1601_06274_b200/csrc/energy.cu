@@ -84,6 +84,24 @@ __global__ void decode_rec_kernel(const uint8_t* __restrict__ rec, const uint8_t
     }
 }
 
+__global__ void decode_dense_kernel(const int32_t* __restrict__ src, const uint8_t* __restrict__ D, int fbits,
+                                    int32_t* __restrict__ dst, long long cells, int K, int KP) {
+    const long long n = cells * K;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long c = i / K;
+        const int k = (int)(i - c * K);
+        int v = src[c * KP + k];
+        if (D) v -= (int)D[c * KP + k] << fbits;
+        dst[i] = v;
+    }
+}
+
+void launch_decode_dense(const int32_t* src, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K, int KP,
+                         cudaStream_t s) {
+    decode_dense_kernel<<<4 * 148, 256, 0, s>>>(src, D, fbits, dst, cells, K, KP);
+}
+
 void launch_decode_rec(const uint8_t* rec, const uint8_t* D, int fbits, int32_t* dst, long long cells, int K,
                        int KP, cudaStream_t s) {
     decode_rec_kernel<<<4 * 148, 256, 0, s>>>(rec, D, fbits, dst, cells, K, KP);

@@ -1,0 +1,350 @@
+// hmg.cu -- Dual MM half-steps for the GENERAL pairwise model (NEXT-3, SURVEY
+// 8(f)): the three-piece penalty of Fig.2 (r = r_{eps,delta} -
+// r_{0,C+delta-eps*delta}, Eq. r-decompose) sampled at integer label
+// differences, times quantised edge-aware weights (Eq. regularizer-form
+// omega_ij "reducing the penalty around sharp edges"):
+//   R(d) = min(e1*min(d,delta) + e2*max(d-delta,0), c)    (units 2^-F)
+//   V_ij(d) = floor(w * om_ij * R(|d|) / 16),   om_ij in [1,16]
+// (readings R29-R31).  Such V is in general NOT a metric (eps < 1 breaks the
+// triangle inequality), so the Handshake keeps Alg.5's literal three Msg
+// (the bounce identity of the truncated-linear kernels does not apply), and
+// every Msg is evaluated from its own edge's weight.
+//
+// Layout: the duals are dense int32 [H][W][KP] (the classic compact u16
+// records' span bound does not hold for arbitrary penalties): gfv = f_ (H
+// output, V input), ggh = D*2^F + g_ (V output, H input).  The hierarchy runs
+// level-synchronously, one warp per (chain, subchain) task; the boundary
+// messages of the subchains of a level live in two int32 [H][W][KP] arrays
+// Lb / Rb at the subchain's first / last node (distinct across a level), so
+// a split writes Rb[i] = phi_ji' (left child) and Lb[j] = phi_ij (right
+// child) and leaves the parent's boundaries in place.  A final kernel emits
+// lambda_p = Lb[p] + F_p + Rb[p] (reading R8) per node: the output record
+// Lb + Rb + D*2^F, the node minimum into the dual bound, and (last V) the
+// lowest-index argmin as the label.
+//
+// Msg over one edge: x is staged in the warp's shared-memory row and every
+// label b takes min(min(x) + V(dc), min_{|d| < dc} x(b+d) + V(|d|)), where dc
+// is the first distance with R(d) = c (V is constant beyond) -- exact.
+#include "ctx.cuh"
+
+namespace dmm {
+
+int genR_host(const dmm_config& c, int d);
+
+namespace {
+
+constexpr int kGW = 4;           // warps per CTA
+constexpr int kBigG = 1 << 29;   // padded labels
+
+struct GenArgs {
+    const uint8_t* D;            // [H][W][KP]
+    const int32_t* src;          // F of the pass ([H][W][KP]), unused when first
+    int32_t* dst;                // output records
+    int32_t* Lb;
+    int32_t* Rb;
+    const uint8_t* om;           // edge weights of this orientation [H][W] (nullptr: 16)
+    uint8_t* labels;
+    long long* bound;
+    int W, H, K, KP, vert, first, last, fbits;
+    int w, e1, e2, delta, c, dc;
+};
+
+__device__ __forceinline__ int genR(const GenArgs& a, int d) {
+    const int lin = a.e1 * min(d, a.delta) + a.e2 * max(d - a.delta, 0);
+    return min(lin, a.c);
+}
+
+template <int LPL>
+struct GenPass {
+    const GenArgs& a;
+    int chain, n, lane;
+    int* sx;                     // this warp's shared row [KP]
+    __device__ GenPass(const GenArgs& a_, int chain_, int lane_, int* sx_) : a(a_), chain(chain_), lane(lane_), sx(sx_) {
+        n = a.vert ? a.H : a.W;
+    }
+    __device__ __forceinline__ size_t q(int p) const {
+        return a.vert ? (size_t)p * a.W + chain : (size_t)chain * a.W + p;
+    }
+    __device__ __forceinline__ int om(int e) const {   // weight of edge (e, e+1) of this chain
+        return a.om ? (int)a.om[q(e)] : 16;
+    }
+    __device__ __forceinline__ void ldF(int p, int (&F)[LPL]) const {
+        const size_t base = q(p) * a.KP + lane * LPL;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            const int k = lane * LPL + e;
+            F[e] = a.first ? ((int)a.D[base + e] << a.fbits) : a.src[base + e];
+            if (k >= a.K) F[e] = kBigG;
+        }
+    }
+    __device__ __forceinline__ void ld(const int32_t* arr, int p, int (&v)[LPL]) const {
+        const size_t base = q(p) * a.KP + lane * LPL;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) v[e] = arr[base + e];
+    }
+    __device__ __forceinline__ void st(int32_t* arr, int p, const int (&v)[LPL]) const {
+        const size_t base = q(p) * a.KP + lane * LPL;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) arr[base + e] = v[e];
+    }
+    // x := Msg over an edge of weight om: out(b) = min_a x(a) + V(|a-b|), exact
+    __device__ __forceinline__ void msg(int (&x)[LPL], int omw) const {
+        int lm = kBigG;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            if (lane * LPL + e >= a.K) x[e] = kBigG;
+            lm = min(lm, x[e]);
+        }
+        const int m = __reduce_min_sync(0xffffffffu, lm);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) sx[lane * LPL + e] = x[e];
+        __syncwarp();
+        const long long wo = (long long)a.w * omw;
+        const int cap = m + (int)((wo * genR(a, a.dc)) >> 4);
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            const int b = lane * LPL + e;
+            int best = cap;
+            if (b < a.K) {
+                best = min(best, x[e]);
+                for (int d = 1; d < a.dc; ++d) {
+                    const int v = (int)((wo * genR(a, d)) >> 4);
+                    if (b - d >= 0) best = min(best, sx[b - d] + v);
+                    if (b + d < a.K) best = min(best, sx[b + d] + v);
+                }
+            }
+            x[e] = best;
+        }
+        __syncwarp();
+    }
+};
+
+// One level of the hierarchy: one warp per (chain, subchain) task.
+template <int LPL>
+__global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev, int ntasks) {
+    extern __shared__ int gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* sx = gsm + warp * 32 * LPL;
+    for (int t = blockIdx.x * kGW + warp; t < ntasks; t += gridDim.x * kGW) {
+        const int chain = t >> lev, s = t & ((1 << lev) - 1);
+        GenPass<LPL> g(a, chain, lane, sx);
+        int lo = 0, hi = g.n - 1;
+        for (int b = lev - 1; b >= 0; --b) {
+            const int mid = lo + (hi - lo + 1) / 2 - 1;
+            if ((s >> b) & 1) lo = mid + 1; else hi = mid;
+        }
+        if (hi <= lo) continue;                       // single node: nothing to split
+        const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
+        int pl[LPL], pr[LPL], F[LPL];
+        if (lev == 0) {
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) { pl[e] = 0; pr[e] = 0; }
+        } else {
+            g.ld(a.Lb, lo, pl);
+            g.ld(a.Rb, hi, pr);
+        }
+        for (int p = lo; p < i; ++p) {               // phi into i from the left (edge p into p+1)
+            g.ldF(p, F);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) pl[e] += F[e];
+            g.msg(pl, g.om(p));
+        }
+        for (int p = hi; p > j; --p) {               // phi into j from the right (edge p-1 into p-1)
+            g.ldF(p, F);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) pr[e] += F[e];
+            g.msg(pr, g.om(p - 1));
+        }
+        // Handshake (Alg.5, literal three Msg; readings R9, R10)
+        const int omij = g.om(i);
+        int pji[LPL], t_[LPL], Fi[LPL];
+        g.ldF(j, F);
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) pji[e] = F[e] + pr[e];
+        g.msg(pji, omij);                                            // phi_ji := Msg(f_j + phi_{j+1,j})
+        g.ldF(i, Fi);
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) t_[e] = (pl[e] + Fi[e] - pji[e]) >> 1;   // floor(m_i/2 - phi_ji)
+        g.msg(t_, omij);                                             // phi_ij
+        int b_[LPL];
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) b_[e] = -t_[e];
+        g.msg(b_, omij);                                             // phi_ji' := Msg(-phi_ij)
+        g.st(a.Rb, i, b_);
+        g.st(a.Lb, j, t_);
+    }
+}
+
+// Chain ends: Lb[first] = Rb[last] = 0 (the boundary messages of level 0).
+__global__ void hmg_ends_kernel(GenArgs a, int chains, int n) {
+    const int KP = a.KP;
+    for (long long z = blockIdx.x * (long long)blockDim.x + threadIdx.x; z < (long long)chains * KP;
+         z += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(z / KP), k = (int)(z - (long long)c * KP);
+        const size_t q0 = a.vert ? (size_t)c : (size_t)c * a.W;
+        const size_t q1 = a.vert ? (size_t)(n - 1) * a.W + c : (size_t)c * a.W + n - 1;
+        a.Lb[q0 * KP + k] = 0;
+        a.Rb[q1 * KP + k] = 0;
+    }
+}
+
+// Leaves: lambda = Lb + F + Rb; record Lb + Rb + D*2^F; bound += min lambda;
+// last V: lowest argmin label.  One warp per node (grid-stride).
+template <int LPL>
+__global__ void __launch_bounds__(kGW * 32) hmg_emit_kernel(GenArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    long long bsum = 0;
+    for (long long qn = gw; qn < (long long)a.W * a.H; qn += nw) {
+        const size_t base = (size_t)qn * a.KP + lane * LPL;
+        int lmin = kBigG, arg = 0x7fffffff;
+        int lam[LPL];
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            const int k = lane * LPL + e;
+            const int Ds = (int)a.D[base + e] << a.fbits;
+            const int F = a.first ? Ds : a.src[base + e];
+            const int lr = a.Lb[base + e] + a.Rb[base + e];
+            lam[e] = lr + F;
+            a.dst[base + e] = k < a.K ? lr + Ds : 0;
+            if (k < a.K) lmin = min(lmin, lam[e]);
+        }
+        const int m = __reduce_min_sync(0xffffffffu, lmin);
+        bsum += m;
+        if (a.last && a.vert) {
+#pragma unroll
+            for (int e = LPL - 1; e >= 0; --e)
+                if (lane * LPL + e < a.K && lam[e] == m) arg = lane * LPL + e;
+            arg = __reduce_min_sync(0xffffffffu, arg);
+            if (lane == 0) a.labels[qn] = (uint8_t)arg;
+        }
+    }
+    if (lane == 0 && bsum != 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.bound), (unsigned long long)bsum);
+}
+
+__global__ void hmg_weights_kernel(const uint8_t* __restrict__ img, long long pitch, int W, int H, const uint8_t* lut,
+                                   uint8_t* om_h, uint8_t* om_v) {
+    for (int qn = blockIdx.x * blockDim.x + threadIdx.x; qn < W * H; qn += gridDim.x * blockDim.x) {
+        const int y = qn / W, x = qn - y * W;
+        const int i = img[(size_t)y * pitch + x];
+        om_h[qn] = x + 1 < W ? lut[abs(i - (int)img[(size_t)y * pitch + x + 1])] : 16;
+        om_v[qn] = y + 1 < H ? lut[abs(i - (int)img[(size_t)(y + 1) * pitch + x])] : 16;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+hmg_energy_kernel(const uint8_t* __restrict__ D, const uint8_t* __restrict__ lab, int W, int H, int K, int KP,
+                  int fbits, int w_h, int w_v, int e1, int e2, int delta, int c, const uint8_t* om_h,
+                  const uint8_t* om_v, long long* energy, int32_t* bad) {
+    long long e = 0;
+    bool oob = false;
+    auto V = [&](int w, int om, int d) -> long long {
+        d = abs(d);
+        const int lin = e1 * min(d, delta) + e2 * max(d - delta, 0);
+        return ((long long)w * om * min(lin, c)) >> 4;
+    };
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < W * H; q += gridDim.x * blockDim.x) {
+        const int y = q / W, x = q - y * W;
+        const int l = lab[q];
+        oob |= l >= K;
+        e += (long long)D[(size_t)q * KP + min(l, K - 1)] << fbits;
+        if (x + 1 < W) e += V(w_h, om_h ? om_h[q] : 16, l - (int)lab[q + 1]);
+        if (y + 1 < H) e += V(w_v, om_v ? om_v[q] : 16, l - (int)lab[q + W]);
+    }
+    if (oob && bad) *bad = 1;
+    for (int d = 16; d > 0; d >>= 1) e += __shfl_down_sync(0xffffffffu, e, d);
+    __shared__ long long part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+        atomicAdd(reinterpret_cast<unsigned long long*>(energy), (unsigned long long)s);
+    }
+}
+
+template <int LPL>
+void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& launches) {
+    hmg_ends_kernel<<<148, 256, 0, s>>>(a, chains, n);
+    int levels = 0;
+    while ((1 << levels) < n) ++levels;          // subchains of length >= 2 exist at levels 0 .. levels-1
+    const int smem = kGW * 32 * LPL * 4;
+    for (int lev = 0; lev < levels; ++lev) {
+        const long long nt = (long long)chains << lev;
+        const int ntasks = (int)nt;
+        int grid = (ntasks + kGW - 1) / kGW;
+        if (grid > 148 * 16) grid = 148 * 16;
+        hmg_level_kernel<LPL><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
+    }
+    hmg_emit_kernel<LPL><<<148 * 8, kGW * 32, 0, s>>>(a);
+    launches += 2 + levels;
+}
+
+}  // namespace
+
+size_t gen_bytes(int W, int H, int KP) { return 2 * (size_t)W * H * KP * 4 + 2 * (size_t)W * H + 256; }
+
+bool gen_mode(const dmm_config* c) {
+    return c->pen_e1 || c->pen_e2 || c->pen_delta || c->pen_c || c->edge_weights;
+}
+
+void gen_weights(dmm_ctx* ctx, int frame, const uint8_t* left, int64_t pitch, cudaStream_t s) {
+    FramePtrs P = frame_ptrs(ctx->L, frame);
+    uint8_t* lut = P.gom_v + (size_t)ctx->L.W * ctx->L.H;
+    hmg_weights_kernel<<<4 * 148, 256, 0, s>>>(left, pitch, ctx->L.W, ctx->L.H, lut, P.gom_h, P.gom_v);
+    ++ctx->launches;
+}
+
+void gen_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations, cudaStream_t s) {
+    const dmm_config& c = ctx->cfg;
+    for (int f = frame; f < frame + nframes; ++f) {
+        FramePtrs P = frame_ptrs(ctx->L, f);
+        GenArgs a;
+        a.D = P.D;
+        a.src = v ? P.gfv : P.ggh;
+        a.dst = v ? P.ggh : P.gfv;
+        a.Lb = P.fwd;
+        a.Rb = P.bwd;
+        a.om = c.edge_weights ? (v ? P.gom_v : P.gom_h) : nullptr;
+        a.labels = P.labels;
+        a.bound = P.bounds + 2 * t + v;
+        a.W = ctx->L.W; a.H = ctx->L.H; a.K = ctx->K; a.KP = ctx->KP;
+        a.vert = v; a.first = (t == 0 && v == 0); a.last = (t == iterations - 1 && v == 1);
+        a.fbits = c.frac_bits;
+        a.w = v ? c.w_v : c.w_h;
+        a.e1 = c.pen_e1; a.e2 = c.pen_e2; a.delta = c.pen_delta; a.c = c.pen_c;
+        int dc = 0;
+        while (dc < ctx->K && genR_host(c, dc) < c.pen_c) ++dc;
+        a.dc = dc;
+        const int chains = v ? a.W : a.H, n = v ? a.H : a.W;
+        switch (ctx->KP / 32) {
+            case 1: run_half<1>(a, chains, n, s, ctx->launches); break;
+            case 2: run_half<2>(a, chains, n, s, ctx->launches); break;
+            case 4: run_half<4>(a, chains, n, s, ctx->launches); break;
+            default: run_half<8>(a, chains, n, s, ctx->launches); break;
+        }
+    }
+}
+
+void gen_energy(dmm_ctx* ctx, int frame, int nframes, const uint8_t* labels, int32_t* bad, cudaStream_t s) {
+    const dmm_config& c = ctx->cfg;
+    for (int f = frame; f < frame + nframes; ++f) {
+        FramePtrs P = frame_ptrs(ctx->L, f);
+        int blocks = (ctx->L.W * ctx->L.H + 255) / 256;
+        if (blocks > 4 * 148) blocks = 4 * 148;
+        hmg_energy_kernel<<<blocks, 256, 0, s>>>(P.D, labels ? labels : P.labels, ctx->L.W, ctx->L.H, ctx->K, ctx->KP,
+                                                 c.frac_bits, c.w_h, c.w_v, c.pen_e1, c.pen_e2, c.pen_delta, c.pen_c,
+                                                 c.edge_weights ? P.gom_h : nullptr, c.edge_weights ? P.gom_v : nullptr,
+                                                 P.energy, bad);
+        ++ctx->launches;
+    }
+}
+
+int genR_host(const dmm_config& c, int d) {
+    const long long lin = (long long)c.pen_e1 * (d < c.pen_delta ? d : c.pen_delta) +
+                          (long long)c.pen_e2 * (d > c.pen_delta ? d - c.pen_delta : 0);
+    return (int)(lin < c.pen_c ? lin : c.pen_c);
+}
+
+}  // namespace dmm

@@ -418,6 +418,10 @@ dmm_status dmm_shard(dmm_ctx* ctx, const uint8_t* id, int rank, int world, int m
             ctx->err = "ROWCOL needs batch == 1 and bands of >= 16 columns and >= 1 row";
             return DMM_E_ARG;
         }
+        if (dmm::gen_mode(&c)) {
+            ctx->err = "ROWCOL is not available for the general pairwise model";
+            return DMM_E_ARG;
+        }
         if (!ctx->pair_ok || !ctx->use_pair) {
             ctx->err = "ROWCOL runs the packed chain-pair kernels: configuration outside their range";
             return DMM_E_ARG;

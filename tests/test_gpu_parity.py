@@ -592,3 +592,73 @@ def test_refine_c2_full_size(orc):
     du = np.abs(u.cpu().numpy().astype(np.float64) - uo)
     assert np.array_equal(u.cpu().numpy(), uo.astype(np.float32)), du.max()
     assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
+
+
+# --------------------------------------- NEXT-3 general penalty + edge weights
+def _gen_case(orc, kind, W, H, K, pen, ew, iters, w_h=2, w_v=3, d_min=0):
+    left, right, _ = datagen.pair(kind, W, H, K, seed=W * H + K)
+    ctx = _ctx(width=W, height=H, d_min=d_min, d_max=d_min + K - 1, w_h=w_h, w_v=w_v, max_iters=iters,
+               pen=pen, edge_weights=ew)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(iters)
+    e, b, hist = ctx.result()
+    g = dict(fdual=ctx.dual(0).cpu().numpy(), gdual=ctx.dual(1).cpu().numpy(),
+             labels=ctx.labels().cpu().numpy().astype(np.int32), bound_hist=np.array(hist, np.int64), energy=e)
+    D = orc.cost_volume(orc.census(left), orc.census(right), d_min, K, 12)
+    oh, ov = orc.edge_weights(left) if ew else (None, None)
+    o = orc.dmm_general(D, w_h, w_v, pen, 4, iters, oh, ov, nthreads=8)
+    return ctx, g, o, D
+
+
+@pytest.mark.parametrize("kind,W,H,K,pen,ew", [
+    ("rd", 70, 30, 16, (8, 16, 2, 80), False),            # eps = 1/2, delta = 2, C = 5
+    ("rd", 45, 33, 32, (4, 16, 1, 48), True),              # edge-aware weights
+    ("wt-kitti", 120, 36, 64, (0, 16, 3, 64), True),       # eps = 0: flat up to delta (P1-P2-like)
+    ("wt-kitti", 90, 21, 128, (12, 16, 1, 96), False),
+    ("rd", 33, 17, 40, (16, 16, 0, 64), False),            # classic shape, padded K
+])
+def test_general_parity(orc, kind, W, H, K, pen, ew):
+    """hmg.cu (general three-piece penalty, per-edge weights, literal Alg.5)
+    == oracle_dmm_general: duals, labels, bound history, energy, bit-exact."""
+    ctx, g, o, D = _gen_case(orc, kind, W, H, K, pen, ew, 3)
+    assert np.array_equal(g["fdual"].astype(np.int64), o["fdual"]), "f_"
+    assert np.array_equal(g["gdual"].astype(np.int64), o["gdual"]), "g_"
+    assert np.array_equal(g["labels"], o["labels"])
+    assert np.array_equal(g["bound_hist"], o["bound_hist"])
+    assert g["energy"] == o["energy"]
+    lab = torch.from_numpy(o["labels"].astype(np.uint8)).cuda()
+    oh, ov = orc.edge_weights(datagen.pair(kind, W, H, K, seed=W * H + K)[0]) if ew else (None, None)
+    assert ctx.energy(labels=lab) == orc.energy_general(D, o["labels"], 2, 3, pen, 4, oh, ov)
+
+
+def test_general_classic_shape_matches_pair_kernels():
+    """General mode with the truncated-linear shape (e1 = e2 = 2^F, c = T 2^F,
+    constant weights) solves the same problem as the packed pair kernels."""
+    W, H, K = 96, 40, 32
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=1)
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    a = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, max_iters=3)
+    b = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, max_iters=3, pen=(16, 16, 0, 64))
+    for c in (a, b):
+        c.cost_volume(lt, rt)
+        c.solve(3)
+    assert a.kernel_family() == "pair"
+    assert a.result() == b.result()
+    assert torch.equal(a.labels(), b.labels()) and torch.equal(a.dual(0), b.dual(0)) and torch.equal(a.dual(1), b.dual(1))
+
+
+def test_general_c2_size_properties():
+    """C2 shape (1242x375x128) with eps = 1/2 penalty and edge-aware weights:
+    the oracle is too slow here, so the properties that hold at any size --
+    monotone bound history, weak duality bound <= E(labels) (Prop.2),
+    energy of the labels by an independent entry point."""
+    W, H, K = 1242, 375, 128
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=0)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w_h=3, w_v=3, max_iters=4, pen=(8, 16, 2, 80),
+               edge_weights=True)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(4)
+    e, b, hist = ctx.result()
+    assert all(x <= y for x, y in zip(hist, hist[1:]))
+    assert b <= e
+    assert ctx.energy(labels=ctx.labels()) == e
