@@ -80,6 +80,14 @@ typedef struct dmm_config {
      * ROWCOL sharding is not available for it. */
     int32_t pen_e1, pen_e2, pen_delta, pen_c;
     int32_t edge_weights;
+    /* Minorant of the chain subproblems (NEXT-4): 0 = hierarchical (Handshake,
+     * P:809-856; the default, "used to obtain all visual experiments"), 1 =
+     * iterative (Alg.4: iter_passes sweeps alternating direction,
+     * lambda_i += floor(m_i / 2^iter_gshift), the last sweep with gamma = 1;
+     * the paper's run max_pass = 3, gamma = 0.25 -> iter_passes 3, iter_gshift 2,
+     * P:804).  The iterative minorant runs on the general int32 kernels (one
+     * warp per chain, sequential along it). */
+    int32_t minorant, iter_passes, iter_gshift;
 } dmm_config;
 
 typedef struct dmm_ctx dmm_ctx;

@@ -59,6 +59,10 @@ def _load():
         lib.oracle_energy_general.argtypes = [P, P, i32, i32, i32, i32, i32, Pen, P, P, i32]
         lib.oracle_energy_general.restype = i64
         lib.oracle_hm_general.argtypes = [P, i32, i32, i32, Pen, P, P]
+        lib.oracle_iter_minorant.argtypes = [P, i32, i32, i32, Pen, P, i32, i32, P]
+        lib.oracle_naive_minorant.argtypes = [P, i32, i32, i32, Pen, P, P]
+        lib.oracle_dmm_minorant.argtypes = [P, i32, i32, i32, i32, i32, Pen, P, P, i32, i32, i32, i32, i32,
+                                            P, P, P, P, P, i32]
         _lib = lib
     return _lib
 
@@ -219,3 +223,41 @@ def energy_general(D, labels, w_h: int, w_v: int, pen, Fbits: int, om_h=None, om
     oh = None if om_h is None else _c(om_h, np.uint8)
     ov = None if om_v is None else _c(om_v, np.uint8)
     return int(_load().oracle_energy_general(_p(D), _p(labels), W, H, K, w_h, w_v, Pen(*pen), _p(oh), _p(ov), Fbits))
+
+
+# ------------------------------------------------------ NEXT-4 minorants
+def iter_minorant(F, w: int, pen, om=None, max_pass: int = 3, gshift: int = 2) -> np.ndarray:
+    F = _c(F, np.int64)
+    n, K = F.shape
+    lam = np.zeros_like(F)
+    omc = None if om is None else _c(om, np.uint8)
+    _load().oracle_iter_minorant(_p(F), n, K, w, Pen(*pen), _p(omc), max_pass, gshift, _p(lam))
+    return lam
+
+
+def naive_minorant(F, w: int, pen, om=None) -> np.ndarray:
+    F = _c(F, np.int64)
+    n, K = F.shape
+    lam = np.zeros_like(F)
+    omc = None if om is None else _c(om, np.uint8)
+    _load().oracle_naive_minorant(_p(F), n, K, w, Pen(*pen), _p(omc), _p(lam))
+    return lam
+
+
+def dmm_minorant(D, w_h: int, w_v: int, pen, Fbits: int, iters: int, minorant: int, max_pass: int = 3,
+                 gshift: int = 2, om_h=None, om_v=None, nthreads: int = 1):
+    """Dual MM with minorant 0 hierarchical / 1 iterative / 2 naive."""
+    D = _c(D, np.uint8)
+    H, W, K = D.shape
+    f = np.zeros((H, W, K), np.int64)
+    g = np.zeros((H, W, K), np.int64)
+    lab = np.zeros((H, W), np.int32)
+    bh = np.zeros(2 * max(iters, 1), np.int64)
+    e = np.zeros(1, np.int64)
+    oh = None if om_h is None else _c(om_h, np.uint8)
+    ov = None if om_v is None else _c(om_v, np.uint8)
+    rc = _load().oracle_dmm_minorant(_p(D), W, H, K, w_h, w_v, Pen(*pen), _p(oh), _p(ov), Fbits, iters, minorant,
+                                     max_pass, gshift, _p(f), _p(g), _p(lab), _p(bh), _p(e), nthreads)
+    if rc:
+        raise ValueError("oracle_dmm_minorant: bad arguments")
+    return dict(fdual=f, gdual=g, labels=lab, bound_hist=bh, energy=int(e[0]))

@@ -17,6 +17,7 @@ static int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 /* floor(x / 2) for any sign (reading R9: "m_i / 2" of Alg.5 P:820 is taken
  * in fixed point with floor). */
 static int64_t floor_half(int64_t x) { return x >= 0 ? x / 2 : -((-x + 1) / 2); }
+static int64_t floor_div(int64_t x, int64_t n) { return x >= 0 ? x / n : -((-x + n - 1) / n); }
 
 static int64_t penalty(int64_t ws, int T, int a, int b) {
     int d = a > b ? a - b : b - a;
@@ -443,10 +444,99 @@ int64_t oracle_energy_general(const uint8_t* D, const int32_t* labels, int W, in
     return e;
 }
 
-/* Algorithm 2 as oracle_dmm, with the general chains. */
+/* NEXT-4 minorants of a chain under the general model (om[n-1] edge weights).
+ * Iterative minorant, Algorithm 4: lambda := 0; for s = 1..max_pass:
+ * for i along the chain, m_i := min-marginal of f - lambda at i computed
+ * dynamically (Eq. msg-pass, min-marginal expression P:646-649),
+ * lambda_i += gamma_s m_i; reverse the chain.  gamma_s = 2^-gshift for
+ * s < max_pass and 1 for the last pass ("For the last pass gamma_s is set to 1
+ * to ensure that the output minorant is maximal"); fixed point:
+ * gamma m = floor(m / 2^gshift) (reading R32).  The first pass runs from node
+ * 0 to node n-1.
+ * Naive minorant: lambda = m / n, the min-marginals of f divided
+ * by the chain length, floor in fixed point (reading R33). */
+static void gen_messages_into(const int64_t* F, const int64_t* lam, int n, int K, const oracle_pen* p, int64_t w,
+                              const uint8_t* om, int dir, int64_t* psi) {
+    /* psi[i] = message into i from the far side (dir = +1: from the right;
+     * dir = -1: from the left) of the chain with unaries F - lam */
+    int64_t* tmp = (int64_t*)malloc((size_t)K * sizeof(int64_t));
+    const int start = dir > 0 ? n - 1 : 0;
+    for (int k = 0; k < K; ++k) psi[(size_t)start * K + k] = 0;
+    for (int i = start - dir; i >= 0 && i < n; i -= dir) {
+        const int src = i + dir, e = dir > 0 ? i : i - 1;   /* edge (i, i+1) or (i-1, i) */
+        for (int k = 0; k < K; ++k)
+            tmp[k] = psi[(size_t)src * K + k] + F[(size_t)src * K + k] - lam[(size_t)src * K + k];
+        gen_msg(tmp, K, p, w, om ? om[e] : 16, &psi[(size_t)i * K]);
+    }
+    free(tmp);
+}
+
+void oracle_iter_minorant(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int max_pass,
+                          int gshift, int64_t* lam) {
+    if (n < 1 || K < 1) return;
+    int64_t* psi = (int64_t*)malloc((size_t)n * K * sizeof(int64_t));
+    int64_t* phi = (int64_t*)malloc((size_t)K * sizeof(int64_t));
+    int64_t* tmp = (int64_t*)malloc((size_t)K * sizeof(int64_t));
+    memset(lam, 0, (size_t)n * K * sizeof(int64_t));
+    for (int s = 0; s < max_pass; ++s) {
+        const int dir = (s % 2 == 0) ? 1 : -1;     /* sweep direction; "Reverse the chain" after each pass */
+        const int sh = (s == max_pass - 1) ? 0 : gshift;
+        gen_messages_into(F, lam, n, K, &pen, w, om, dir, psi);   /* far side, current remainder */
+        for (int k = 0; k < K; ++k) phi[k] = 0;
+        const int first = dir > 0 ? 0 : n - 1;
+        for (int i = first; i >= 0 && i < n; i += dir) {
+            for (int k = 0; k < K; ++k) {
+                const size_t q = (size_t)i * K + k;
+                const int64_t m = phi[k] + F[q] - lam[q] + psi[q];            /* min-marginal of f - lambda at i */
+                lam[q] += sh ? (m >> sh) : m;                                 /* lambda_i += gamma_s m_i (R32) */
+            }
+            if (i + dir >= 0 && i + dir < n) {
+                const int e = dir > 0 ? i : i - 1;
+                for (int k = 0; k < K; ++k) tmp[k] = phi[k] + F[(size_t)i * K + k] - lam[(size_t)i * K + k];
+                gen_msg(tmp, K, &pen, w, om ? om[e] : 16, phi);
+            }
+        }
+    }
+    free(psi); free(phi); free(tmp);
+}
+
+void oracle_naive_minorant(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int64_t* lam) {
+    if (n < 1 || K < 1) return;
+    int64_t* zero = (int64_t*)calloc((size_t)n * K, sizeof(int64_t));
+    int64_t* L = (int64_t*)malloc((size_t)n * K * sizeof(int64_t));
+    int64_t* R = (int64_t*)malloc((size_t)n * K * sizeof(int64_t));
+    gen_messages_into(F, zero, n, K, &pen, w, om, -1, L);
+    gen_messages_into(F, zero, n, K, &pen, w, om, 1, R);
+    for (size_t q = 0; q < (size_t)n * K; ++q) lam[q] = floor_div(L[q] + F[q] + R[q], n);
+    free(zero); free(L); free(R);
+}
+
+static void chain_minorant(int minorant, const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om,
+                           int max_pass, int gshift, int64_t* lam) {
+    if (minorant == 1) oracle_iter_minorant(F, n, K, w, pen, om, max_pass, gshift, lam);
+    else if (minorant == 2) oracle_naive_minorant(F, n, K, w, pen, om, lam);
+    else oracle_hm_general(F, n, K, w, pen, om, lam);
+}
+
+/* Algorithm 2 as oracle_dmm, with the general chains and a choice
+ * of minorant (0 hierarchical, 1 iterative, 2 naive). */
+int oracle_dmm_minorant(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
+                        const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int minorant, int max_pass,
+                        int gshift, int64_t* fdual, int64_t* gdual, int32_t* labels, int64_t* bound_hist,
+                        int64_t* energy, int nthreads);
+
 int oracle_dmm_general(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
                        const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int64_t* fdual,
                        int64_t* gdual, int32_t* labels, int64_t* bound_hist, int64_t* energy, int nthreads) {
+    return oracle_dmm_minorant(D, W, H, K, w_h, w_v, pen, om_h, om_v, Fbits, iters, 0, 0, 0, fdual, gdual, labels,
+                               bound_hist, energy, nthreads);
+}
+
+int oracle_dmm_minorant(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
+                        const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int minorant, int max_pass,
+                        int gshift, int64_t* fdual, int64_t* gdual, int32_t* labels, int64_t* bound_hist,
+                        int64_t* energy, int nthreads) {
+    if (minorant < 0 || minorant > 2 || (minorant == 1 && (max_pass < 1 || gshift < 0 || gshift > 30))) return 1;
     if (!D || W < 1 || H < 1 || K < 1 || K > 256 || w_h < 0 || w_v < 0 || pen.e1 < 0 || pen.e2 < pen.e1 ||
         pen.delta < 0 || pen.c < 0 || Fbits < 0 || Fbits > 16 || iters < 1)
         return 1;
@@ -476,7 +566,7 @@ int oracle_dmm_general(const uint8_t* D, int W, int H, int K, int w_h, int w_v, 
                     Fr[(size_t)x * K + k] = (int64_t)D[q] * scale + g[q];
                 }
             }
-            oracle_hm_general(Fr, W, K, w_h, pen, om, h);
+            chain_minorant(minorant, Fr, W, K, w_h, pen, om, max_pass, gshift, h);
             for (int x = 0; x < W; ++x) {
                 int64_t mn = h[(size_t)x * K];
                 for (int k = 0; k < K; ++k) {
@@ -499,7 +589,7 @@ int oracle_dmm_general(const uint8_t* D, int W, int H, int K, int w_h, int w_v, 
                 om[y] = om_v ? om_v[(size_t)y * W + x] : 16;
                 for (int k = 0; k < K; ++k) Gc[(size_t)y * K + k] = f[((size_t)y * W + x) * K + k];
             }
-            oracle_hm_general(Gc, H, K, w_v, pen, om, v);
+            chain_minorant(minorant, Gc, H, K, w_v, pen, om, max_pass, gshift, v);
             for (int y = 0; y < H; ++y) {
                 int64_t mn = v[(size_t)y * K];
                 int32_t arg = 0;

@@ -123,6 +123,22 @@ int64_t oracle_energy_general(const uint8_t* D, const int32_t* labels, int W, in
  * weights (nullable = 16), w the direction weight. */
 void oracle_hm_general(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int64_t* lam);
 
+/* ---- NEXT-4 minorant variants (readings R32, R33).
+ * Iterative minorant, Alg.4: max_pass passes alternating
+ * direction (first: node 0 -> n-1), lambda_i += floor(m_i / 2^gshift) with the
+ * dynamic min-marginal m_i of f - lambda, the last pass with gamma = 1
+ * (the paper's run: max_pass = 3, gamma = 0.25).
+ * Naive minorant: lambda = floor(min-marginals of f / n). */
+void oracle_iter_minorant(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int max_pass,
+                          int gshift, int64_t* lam);
+void oracle_naive_minorant(const int64_t* F, int n, int K, int w, oracle_pen pen, const uint8_t* om, int64_t* lam);
+/* Dual MM with minorant 0 = hierarchical (= oracle_dmm_general), 1 =
+ * iterative (max_pass, gshift), 2 = naive. */
+int oracle_dmm_minorant(const uint8_t* D, int W, int H, int K, int w_h, int w_v, oracle_pen pen,
+                        const uint8_t* om_h, const uint8_t* om_v, int Fbits, int iters, int minorant, int max_pass,
+                        int gshift, int64_t* fdual, int64_t* gdual, int32_t* labels, int64_t* bound_hist,
+                        int64_t* energy, int nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,7 +46,8 @@ class DmmError(RuntimeError):
 class DmmConfig(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "width", "height", "d_min", "d_max", "census_radius", "w_h", "w_v", "trunc",
-        "frac_bits", "oob_cost", "batch", "max_iters", "pen_e1", "pen_e2", "pen_delta", "pen_c", "edge_weights")]
+        "frac_bits", "oob_cost", "batch", "max_iters", "pen_e1", "pen_e2", "pen_delta", "pen_c", "edge_weights",
+        "minorant", "iter_passes", "iter_gshift")]
 
 
 class DmmRefineParams(ctypes.Structure):
@@ -61,10 +62,13 @@ class DmmXfer(ctypes.Structure):
 
 
 def make_config(width, height, d_min=0, d_max=127, w=3, T=4, frac_bits=4, census_radius=2, oob_cost=-1,
-                batch=1, max_iters=16, w_h=None, w_v=None, pen=None, edge_weights=False) -> DmmConfig:
+                batch=1, max_iters=16, w_h=None, w_v=None, pen=None, edge_weights=False, minorant="hierarchical",
+                iter_passes=3, iter_gshift=2) -> DmmConfig:
     p = pen if pen is not None else (0, 0, 0, 0)
+    mi = {"hierarchical": 0, "iterative": 1}[minorant]
     return DmmConfig(width, height, d_min, d_max, census_radius, w if w_h is None else w_h,
-                     w if w_v is None else w_v, T, frac_bits, oob_cost, batch, max_iters, *p, int(bool(edge_weights)))
+                     w if w_v is None else w_v, T, frac_bits, oob_cost, batch, max_iters, *p, int(bool(edge_weights)),
+                     mi, iter_passes if mi else 0, iter_gshift if mi else 0)
 
 
 def library_path() -> str:
@@ -201,14 +205,15 @@ class Context:
     def __init__(self, width: int, height: int, d_min: int = 0, d_max: int = 127, w: int = 3,
                  T: int = 4, frac_bits: int = 4, census_radius: int = 2, oob_cost: int = -1,
                  batch: int = 1, max_iters: int = 16, w_h: int | None = None,
-                 w_v: int | None = None, device=None, shard_world: int = 0, pen=None, edge_weights: bool = False):
+                 w_v: int | None = None, device=None, shard_world: int = 0, pen=None, edge_weights: bool = False,
+                 minorant: str = "hierarchical", iter_passes: int = 3, iter_gshift: int = 2):
         import torch
         if not torch.cuda.is_available():
             raise DmmError("no CUDA device: the DMM hot path has no CPU fallback")
         self._lib = load_library()
         self.device = torch.device(device if device is not None else f"cuda:{torch.cuda.current_device()}")
         self.cfg = make_config(width, height, d_min, d_max, w, T, frac_bits, census_radius, oob_cost, batch,
-                               max_iters, w_h, w_v, pen, edge_weights)
+                               max_iters, w_h, w_v, pen, edge_weights, minorant, iter_passes, iter_gshift)
         self.W, self.H, self.K = width, height, d_max - d_min + 1
         self.batch, self.frac_bits, self.max_iters = batch, frac_bits, max_iters
         nbytes = self._lib.dmm_workspace_bytes(ctypes.byref(self.cfg))

@@ -24,6 +24,9 @@ bool valid(const dmm_config* c) {
     if (c->pen_e1 < 0 || c->pen_e2 < c->pen_e1 || c->pen_delta < 0 || c->pen_c < 0 || c->pen_c > (1 << 20) ||
         c->pen_e2 > (1 << 20) || (c->edge_weights != 0 && c->edge_weights != 1))
         return false;
+    if (c->minorant < 0 || c->minorant > 1 ||
+        (c->minorant == 1 && (c->iter_passes < 1 || c->iter_passes > 64 || c->iter_gshift < 0 || c->iter_gshift > 16)))
+        return false;
     const int K = c->d_max - c->d_min + 1;
     // width <= 16384: cost_kernel stages the row's two code rows (8 * W bytes) in
     // shared memory; W * H <= 2^28 keeps every pixel index in int32.
@@ -237,7 +240,9 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
         const long long maxD = (cfg->oob_cost > bits ? cfg->oob_cost : bits) << cfg->frac_bits;
         const long long w = cfg->w_h > cfg->w_v ? cfg->w_h : cfg->w_v;
         const long long n = cfg->width > cfg->height ? cfg->width : cfg->height;
-        if (4 * n * (maxD + 2 * w * cfg->pen_c) >= (1ll << 30)) return DMM_E_RANGE;
+        const long long cap = (cfg->pen_e1 || cfg->pen_e2 || cfg->pen_delta || cfg->pen_c)
+                                  ? cfg->pen_c : ((long long)cfg->trunc << cfg->frac_bits);
+        if (4 * n * (maxD + 2 * w * cap) >= (1ll << 30)) return DMM_E_RANGE;
     } else if (span_bound(cfg) > 65535) {
         return DMM_E_RANGE;
     }

@@ -30,6 +30,7 @@
 namespace dmm {
 
 int genR_host(const dmm_config& c, int d);
+void pen_of(const dmm_config& c, int& e1, int& e2, int& delta, int& cc);
 
 namespace {
 
@@ -47,6 +48,7 @@ struct GenArgs {
     long long* bound;
     int W, H, K, KP, vert, first, last, fbits;
     int w, e1, e2, delta, c, dc;
+    int passes, gshift;          // iterative minorant (NEXT-4)
 };
 
 __device__ __forceinline__ int genR(const GenArgs& a, int d) {
@@ -191,7 +193,7 @@ __global__ void hmg_ends_kernel(GenArgs a, int chains, int n) {
 
 // Leaves: lambda = Lb + F + Rb; record Lb + Rb + D*2^F; bound += min lambda;
 // last V: lowest argmin label.  One warp per node (grid-stride).
-template <int LPL>
+template <int LPL, bool DIRECT>
 __global__ void __launch_bounds__(kGW * 32) hmg_emit_kernel(GenArgs a) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -205,7 +207,8 @@ __global__ void __launch_bounds__(kGW * 32) hmg_emit_kernel(GenArgs a) {
             const int k = lane * LPL + e;
             const int Ds = (int)a.D[base + e] << a.fbits;
             const int F = a.first ? Ds : a.src[base + e];
-            const int lr = a.Lb[base + e] + a.Rb[base + e];
+            // hierarchical: lambda = Lb + F + Rb (leaf, R8); iterative: lambda = Rb
+            const int lr = DIRECT ? a.Rb[base + e] - F : a.Lb[base + e] + a.Rb[base + e];
             lam[e] = lr + F;
             a.dst[base + e] = k < a.K ? lr + Ds : 0;
             if (k < a.K) lmin = min(lmin, lam[e]);
@@ -277,8 +280,73 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
         if (grid > 148 * 16) grid = 148 * 16;
         hmg_level_kernel<LPL><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
     }
-    hmg_emit_kernel<LPL><<<148 * 8, kGW * 32, 0, s>>>(a);
+    hmg_emit_kernel<LPL, false><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2 + levels;
+}
+
+// Iterative minorant (Alg.4, readings R32): one warp per chain,
+// `passes` sweeps alternating direction (the first from node 0), each
+// preceded by the far-side messages of the current remainder f - lambda
+// (stored in Lb); lambda (in Rb) += floor(m_i / 2^gshift) with the dynamic
+// min-marginal m_i, the last pass with gamma = 1.
+template <int LPL>
+__global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chains) {
+    extern __shared__ int gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* sx = gsm + warp * 32 * LPL;
+    for (int ch = blockIdx.x * kGW + warp; ch < chains; ch += gridDim.x * kGW) {
+        GenPass<LPL> g(a, ch, lane, sx);
+        const int n = g.n;
+        int z[LPL];
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) z[e] = 0;
+        for (int p = 0; p < n; ++p) g.st(a.Rb, p, z);
+        for (int s = 0; s < a.passes; ++s) {
+            const int dir = (s & 1) ? -1 : 1;
+            const int sh = s == a.passes - 1 ? 0 : a.gshift;
+            const int start = dir > 0 ? n - 1 : 0;          // far end
+            int psi[LPL], F[LPL], lam[LPL];
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) psi[e] = 0;
+            g.st(a.Lb, start, psi);
+            for (int i = start - dir; i >= 0 && i < n; i -= dir) {
+                const int src = i + dir;
+                g.ldF(src, F);
+                g.ld(a.Rb, src, lam);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) psi[e] += F[e] - lam[e];
+                g.msg(psi, g.om(dir > 0 ? i : i - 1));
+                g.st(a.Lb, i, psi);
+            }
+            int phi[LPL];
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) phi[e] = 0;
+            for (int i = dir > 0 ? 0 : n - 1; i >= 0 && i < n; i += dir) {
+                g.ldF(i, F);
+                g.ld(a.Rb, i, lam);
+                g.ld(a.Lb, i, psi);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) {
+                    const int m = phi[e] + F[e] - lam[e] + psi[e];     // min-marginal of f - lambda at i
+                    lam[e] += sh ? (m >> sh) : m;
+                }
+                g.st(a.Rb, i, lam);
+                if (i + dir >= 0 && i + dir < n) {
+#pragma unroll
+                    for (int e = 0; e < LPL; ++e) phi[e] += F[e] - lam[e];
+                    g.msg(phi, g.om(dir > 0 ? i : i - 1));
+                }
+            }
+        }
+    }
+}
+
+template <int LPL>
+void run_iter(const GenArgs& a, int chains, cudaStream_t s, long long& launches) {
+    int grid = (chains + kGW - 1) / kGW;
+    hmg_iter_kernel<LPL><<<grid, kGW * 32, kGW * 32 * LPL * 4, s>>>(a, chains);
+    hmg_emit_kernel<LPL, true><<<148 * 8, kGW * 32, 0, s>>>(a);
+    launches += 2;
 }
 
 }  // namespace
@@ -286,7 +354,7 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
 size_t gen_bytes(int W, int H, int KP) { return 2 * (size_t)W * H * KP * 4 + 2 * (size_t)W * H + 256; }
 
 bool gen_mode(const dmm_config* c) {
-    return c->pen_e1 || c->pen_e2 || c->pen_delta || c->pen_c || c->edge_weights;
+    return c->pen_e1 || c->pen_e2 || c->pen_delta || c->pen_c || c->edge_weights || c->minorant;
 }
 
 void gen_weights(dmm_ctx* ctx, int frame, const uint8_t* left, int64_t pitch, cudaStream_t s) {
@@ -313,11 +381,21 @@ void gen_half(dmm_ctx* ctx, int frame, int nframes, int t, int v, int iterations
         a.vert = v; a.first = (t == 0 && v == 0); a.last = (t == iterations - 1 && v == 1);
         a.fbits = c.frac_bits;
         a.w = v ? c.w_v : c.w_h;
-        a.e1 = c.pen_e1; a.e2 = c.pen_e2; a.delta = c.pen_delta; a.c = c.pen_c;
+        pen_of(c, a.e1, a.e2, a.delta, a.c);
         int dc = 0;
-        while (dc < ctx->K && genR_host(c, dc) < c.pen_c) ++dc;
+        while (dc < ctx->K && genR_host(c, dc) < a.c) ++dc;
         a.dc = dc;
+        a.passes = c.iter_passes; a.gshift = c.iter_gshift;
         const int chains = v ? a.W : a.H, n = v ? a.H : a.W;
+        if (c.minorant == 1) {
+            switch (ctx->KP / 32) {
+                case 1: run_iter<1>(a, chains, s, ctx->launches); break;
+                case 2: run_iter<2>(a, chains, s, ctx->launches); break;
+                case 4: run_iter<4>(a, chains, s, ctx->launches); break;
+                default: run_iter<8>(a, chains, s, ctx->launches); break;
+            }
+            continue;
+        }
         switch (ctx->KP / 32) {
             case 1: run_half<1>(a, chains, n, s, ctx->launches); break;
             case 2: run_half<2>(a, chains, n, s, ctx->launches); break;
@@ -333,18 +411,32 @@ void gen_energy(dmm_ctx* ctx, int frame, int nframes, const uint8_t* labels, int
         FramePtrs P = frame_ptrs(ctx->L, f);
         int blocks = (ctx->L.W * ctx->L.H + 255) / 256;
         if (blocks > 4 * 148) blocks = 4 * 148;
+        int e1, e2, dl, cc;
+        pen_of(c, e1, e2, dl, cc);
         hmg_energy_kernel<<<blocks, 256, 0, s>>>(P.D, labels ? labels : P.labels, ctx->L.W, ctx->L.H, ctx->K, ctx->KP,
-                                                 c.frac_bits, c.w_h, c.w_v, c.pen_e1, c.pen_e2, c.pen_delta, c.pen_c,
+                                                 c.frac_bits, c.w_h, c.w_v, e1, e2, dl, cc,
                                                  c.edge_weights ? P.gom_h : nullptr, c.edge_weights ? P.gom_v : nullptr,
                                                  P.energy, bad);
         ++ctx->launches;
     }
 }
 
+// The penalty of the general kernels: the config's, or (all zero: the classic
+// model in general storage, e.g. for the iterative minorant) e1 = e2 = 2^F,
+// delta = 0, c = T 2^F, i.e. V = w min(|d|, T) 2^F with om = 16.
+void pen_of(const dmm_config& c, int& e1, int& e2, int& delta, int& cc) {
+    if (c.pen_e1 || c.pen_e2 || c.pen_delta || c.pen_c) {
+        e1 = c.pen_e1; e2 = c.pen_e2; delta = c.pen_delta; cc = c.pen_c;
+    } else {
+        e1 = e2 = 1 << c.frac_bits; delta = 0; cc = c.trunc << c.frac_bits;
+    }
+}
+
 int genR_host(const dmm_config& c, int d) {
-    const long long lin = (long long)c.pen_e1 * (d < c.pen_delta ? d : c.pen_delta) +
-                          (long long)c.pen_e2 * (d > c.pen_delta ? d - c.pen_delta : 0);
-    return (int)(lin < c.pen_c ? lin : c.pen_c);
+    int e1, e2, delta, cc;
+    pen_of(c, e1, e2, delta, cc);
+    const long long lin = (long long)e1 * (d < delta ? d : delta) + (long long)e2 * (d > delta ? d - delta : 0);
+    return (int)(lin < cc ? lin : cc);
 }
 
 }  // namespace dmm

@@ -662,3 +662,29 @@ def test_general_c2_size_properties():
     assert all(x <= y for x, y in zip(hist, hist[1:]))
     assert b <= e
     assert ctx.energy(labels=ctx.labels()) == e
+
+
+# ------------------------------------------- NEXT-4 iterative minorant (Alg.4)
+@pytest.mark.parametrize("kind,W,H,K,pen,ew,passes,gshift", [
+    ("rd", 64, 48, 16, None, False, 3, 2),                # configs[0] shape, the paper's max_pass = 3, gamma = 1/4
+    ("wt-kitti", 90, 31, 32, (8, 16, 2, 80), True, 3, 2),
+    ("rd", 37, 29, 40, None, False, 4, 1),
+    ("wt-kitti", 50, 20, 128, None, False, 1, 2),         # max_pass 1: one full (gamma = 1) pass
+])
+def test_iterative_minorant_parity(orc, kind, W, H, K, pen, ew, passes, gshift):
+    """Dual MM with the iterative minorant on the GPU (one warp per chain)
+    == oracle_dmm_minorant(minorant = 1): duals, labels, bounds, energy."""
+    iters = 3
+    left, right, _ = datagen.pair(kind, W, H, K, seed=K + W)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w_h=2, w_v=3, T=4, max_iters=iters, pen=pen,
+               edge_weights=ew, minorant="iterative", iter_passes=passes, iter_gshift=gshift)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(iters)
+    e, b, hist = ctx.result()
+    D = orc.cost_volume(orc.census(left), orc.census(right), 0, K, 12)
+    oh, ov = orc.edge_weights(left) if ew else (None, None)
+    o = orc.dmm_minorant(D, 2, 3, pen or (16, 16, 0, 64), 4, iters, 1, passes, gshift, oh, ov, nthreads=8)
+    assert np.array_equal(ctx.dual(0).cpu().numpy().astype(np.int64), o["fdual"])
+    assert np.array_equal(ctx.dual(1).cpu().numpy().astype(np.int64), o["gdual"])
+    assert np.array_equal(ctx.labels().cpu().numpy().astype(np.int32), o["labels"])
+    assert hist == [int(v) for v in o["bound_hist"]] and e == o["energy"]
