@@ -206,6 +206,8 @@ def main():
                     help="NEXT-3 general penalty e1,e2,delta,c (units 2^-F, e.g. 8,16,2,80: eps=1/2, delta=2, C=5) "
                          "solved by the general int32 kernels")
     ap.add_argument("--edge-weights", action="store_true", help="NEXT-3 edge-aware pairwise weights")
+    ap.add_argument("--minorant", choices=("hierarchical", "iterative"), default="hierarchical",
+                    help="NEXT-4: chain minorant (iterative = Alg.4, max_pass 3, gamma 1/4)")
     ap.add_argument("--refine", action="store_true",
                     help="append the continuous refinement (NEXT-2: 5 warps x 40 PDHG iterations, P:497) to every "
                          "step (frames mode, one frame per GPU)")
@@ -242,7 +244,8 @@ def main():
     left, right = distinct[0][0], distinct[0][1]
     pen = tuple(int(v) for v in args.pen.split(",")) if args.pen else None
     ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=W_REG, T=T_REG, frac_bits=FBITS,
-                      max_iters=iters, batch=nf, device=dev, pen=pen, edge_weights=args.edge_weights)
+                      max_iters=iters, batch=nf, device=dev, pen=pen, edge_weights=args.edge_weights,
+                      minorant=args.minorant)
     Lh = np.stack([distinct[s % len(distinct)][0] for s in range(nf)])
     Rh = np.stack([distinct[s % len(distinct)][1] for s in range(nf)])
     lt = torch.from_numpy(Lh).to(dev)
@@ -395,6 +398,7 @@ def main():
                        "pairwise": ("general penalty e1,e2,delta,c=" + args.pen if args.pen else
                                     f"truncated linear w={W_REG}, T={T_REG}")
                                    + (", edge-aware weights" if args.edge_weights else ""),
+                       "minorant": args.minorant,
                        "fps": world * nf / (ms / 1e3), "parallelism": f"frames x{world}",
                        "l2": "flushed between timed steps (256 MB write outside events); step working set ~1 GB"},
             "roofline": roofline,
