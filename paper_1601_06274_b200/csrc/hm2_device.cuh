@@ -141,67 +141,6 @@ __device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], const DtK<LPL>& 
     return G;
 }
 
-// The distance transform split in its two independent halves, for the
-// latency-bound long passes (Task::run_pass): Msg(x) = min(Wn(x), min(x) + wsT)
-// where Wn is the windowed lower envelope without the truncation cap (exact:
-// every candidate at distance >= T is >= min(x) + wsT).  A pass keeps
-// phi = min(y, cap) with y = Wn(x) and the per-chain cap applied lazily at the
-// start of the next step, so the warp reduction of min(x) (CREDUX) runs
-// concurrently with Wn(x) instead of feeding the step's last instruction.
-// Returns pk(min A, min B) of x; x is masked (PAD) in place.
-template <int LPL, bool PAD>
-__device__ __forceinline__ unsigned dt2_min(unsigned (&x)[LPL], const DtK<LPL>& k, int& gA, int& gB) {
-    if constexpr (PAD) {
-#pragma unroll
-        for (int e = 0; e < LPL; ++e)
-            if (k.lane * LPL + e >= k.K) x[e] = kBigP;
-    }
-    unsigned lred = x[0];
-#pragma unroll
-    for (int e = 1; e < LPL; ++e) lred = __vmins2(lred, x[e]);
-    gA = __reduce_min_sync(kFull, lo16(lred));
-    gB = __reduce_min_sync(kFull, hi16(lred));
-    return pk(gA, gB);
-}
-// x := Wn(x) (no cap), x already PAD-masked by dt2_min
-template <int LPL, int WIN>
-__device__ __forceinline__ void dt2_window(unsigned (&x)[LPL], const DtK<LPL>& k) {
-    unsigned fw[LPL], bw[LPL];
-    fw[0] = x[0];
-#pragma unroll
-    for (int e = 1; e < LPL; ++e) fw[e] = __viaddmin_s16x2(fw[e - 1], k.wsP, x[e]);
-    bw[LPL - 1] = x[LPL - 1];
-#pragma unroll
-    for (int e = LPL - 2; e >= 0; --e) bw[e] = __viaddmin_s16x2(bw[e + 1], k.wsP, x[e]);
-    unsigned inf, inb;
-    if constexpr (WIN != 0) {
-        inf = __shfl_up_sync(kFull, fw[LPL - 1], 1);
-        inb = __shfl_down_sync(kFull, bw[0], 1);
-    } else {
-        unsigned cf = fw[LPL - 1], cb = bw[0];
-        const int clampv = k.wsT + 1;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int st = min(k.ws * LPL * d, clampv);
-            const unsigned stP = pk(st, st);
-            const unsigned tf = __shfl_up_sync(kFull, cf, d);
-            const unsigned tb = __shfl_down_sync(kFull, cb, d);
-            if (k.lane >= d) cf = __viaddmin_s16x2(tf, stP, cf);
-            if (k.lane + d < 32) cb = __viaddmin_s16x2(tb, stP, cb);
-        }
-        inf = __shfl_up_sync(kFull, cf, 1);
-        inb = __shfl_down_sync(kFull, cb, 1);
-    }
-#pragma unroll
-    for (int e = 0; e < LPL; ++e) {
-        const bool needL = WIN > 0 ? (e + 1 < WIN) : true;
-        const bool needR = WIN > 0 ? (LPL - e < WIN) : true;
-        const unsigned vf = needL ? __viaddmin_s16x2(inf, k.aL[e], fw[e]) : fw[e];
-        const unsigned vb = needR ? __viaddmin_s16x2(inb, k.aR[e], bw[e]) : bw[e];
-        x[e] = __vmins2(vf, vb);
-    }
-}
-
 // ---- message pairs: packed normalised values + per-chain offsets
 template <int LPL>
 struct MP {
