@@ -17,6 +17,17 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 c = datagen.CONFIGS[cfg]
 W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
+if c["kind"] == "flow":                       # configs[3]: two K-label layers of one context
+    i1, i2, _, _ = datagen.flow_pair(W, H, -c["d_min"], seed=0)
+    ctx = dmm.Context(width=W, height=H, d_min=c["d_min"], d_max=c["d_min"] + K - 1, w=3, T=4, frac_bits=4,
+                      max_iters=iters, batch=2)
+    t1, t2 = torch.from_numpy(i1).cuda(), torch.from_numpy(i2).cuda()
+    for _ in range(reps):
+        ctx.flow_cost_volume(t1, t2, c["d_min"])
+        ctx.solve(iters, nframes=2)
+    torch.cuda.synchronize()
+    print(cfg, ctx.result(0), ctx.result(1))
+    sys.exit(0)
 nf = c.get("frames", 1)
 pairs = [datagen.pair(c["kind"], W, H, K, seed=s) for s in range(min(nf, 8))]
 lt = torch.stack([torch.from_numpy(pairs[s % len(pairs)][0]) for s in range(nf)]).cuda()
