@@ -22,10 +22,29 @@ namespace p2 {
 constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
 constexpr int kDepth = 2;    // pending right pieces in a leaf block (pieces >= 4 nodes push; 12 -> 6 -> 3)
 static_assert(kCMax <= 15, "leaf stack depth 2");
-template <int LPL> constexpr int nwg() { return 2; }   // warps per CTA, level kernels: small CTAs spread the few tasks of the top levels over all SMs
-constexpr int kNWL = 8;      // warps per CTA, leaf kernel
-constexpr int kRootCH = 16, kRootNS = 2;
-constexpr int kLevCH = 8, kLevNS = 2;
+// Tuning constants (overridable with -D for experiments; the defaults are the measured best)
+#ifndef DMM_NWG
+#define DMM_NWG 2
+#endif
+#ifndef DMM_NWL
+#define DMM_NWL 4
+#endif
+#ifndef DMM_ROOT_CH
+#define DMM_ROOT_CH 16
+#endif
+#ifndef DMM_LEV_CH
+#define DMM_LEV_CH 8
+#endif
+#ifndef DMM_LEV_NS
+#define DMM_LEV_NS 2
+#endif
+#ifndef DMM_LEAF_MINB
+#define DMM_LEAF_MINB 1
+#endif
+template <int LPL> constexpr int nwg() { return DMM_NWG; }   // warps per CTA, level kernels: small CTAs spread the few tasks of the top levels over all SMs
+constexpr int kNWL = DMM_NWL;      // warps per CTA, leaf kernel
+constexpr int kRootCH = DMM_ROOT_CH, kRootNS = 2;
+constexpr int kLevCH = DMM_LEV_CH, kLevNS = DMM_LEV_NS;
 #ifndef DMM_LEV_MIN_CTAS
 #define DMM_LEV_MIN_CTAS 12
 #endif
@@ -512,7 +531,7 @@ __device__ __forceinline__ void leaf_emit(const Pass<LPL, VERT, PAD, WIN, FIRST>
 // block's record pairs, D rows and boundary messages, then solve its
 // sub-hierarchy on chip, depth first (as hm_leaf_kernel in hm.cu).
 template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST>
-__global__ void __launch_bounds__(kNWL * 32) hm2_leaf_kernel(PassArgs a, int lstar, int nblocks) {
+__global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(PassArgs a, int lstar, int nblocks) {
     extern __shared__ __align__(128) char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     using PS = Pass<LPL, VERT, PAD, WIN, FIRST>;
