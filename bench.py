@@ -29,6 +29,9 @@ import numpy as np  # noqa: E402
 
 import datagen  # noqa: E402
 
+# one JSON line on stdout: keep NCCL's banner off stdout unless the caller asks for it
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+
 METRIC = "cost-volume cell-iterations/s (1242x375x128, 4 dual iterations)"
 
 

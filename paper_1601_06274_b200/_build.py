@@ -8,7 +8,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "_lib", "libdmm_b200.so")
+LIB = os.environ.get("DMM_B200_LIB_OUT") or os.path.join(HERE, "_lib", "libdmm_b200.so")
+EXTRA = os.environ.get("DMM_NVCC_EXTRA", "").split()     # experiment variants (-D...)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -40,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     tag = f"tmp{os.getpid()}"
     objs = [os.path.join(os.path.dirname(LIB), os.path.basename(src)[:-3] + f".{tag}.o") for src in sources()]
-    comp = [f for f in FLAGS if f != "-shared"]
+    comp = [f for f in FLAGS if f != "-shared"] + EXTRA
     # one nvcc per translation unit, in parallel (the chain-DP units dominate)
     procs = [subprocess.Popen([NVCC, *comp, *FILE_FLAGS.get(os.path.basename(src), []), "-c", "-o", o, src],
                               stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
