@@ -97,6 +97,7 @@ size_t frame_layout(const dmm_config* c, dmm::FramePtrs* off) {
     off->bounds = (long long*)take(8 * 2 * (size_t)c->max_iters);
     off->energy = (long long*)take(8);
     off->flag = (int32_t*)take(8);
+    off->tmap = (uint8_t*)take(dmm::kTmapBytes);
     off->rf = (float*)take(dmm::refine_bytes((int)W, (int)H));
     off->renergy = (double*)take(8);
     if (dmm::gen_mode(c)) {
@@ -188,6 +189,7 @@ dmm_status launch_half_on(dmm_ctx* ctx, const Layout& L, int frame, int nframes,
     a.bound_slot = 2 * t + v;
     a.nseg = nseg;
     a.segx = segx;
+    a.vtma = (&L == &ctx->sh.Lv) ? ctx->sh.vtma : ctx->vtma;
     if (gen_mode(&ctx->cfg)) {
         Timed tm(ctx, 2 + v, s, 0);
         gen_half(ctx, frame, nframes, t, v, iterations, s);
@@ -275,6 +277,7 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     c->L.base.energy = (long long*)(b + (size_t)off.energy);
     c->L.base.flag = (int32_t*)(b + (size_t)off.flag);
     c->L.base.rf = (float*)(b + (size_t)off.rf);
+    c->L.base.tmap = (uint8_t*)(b + (size_t)off.tmap);
     c->L.base.renergy = (double*)(b + (size_t)off.renergy);
     c->L.base.gfv = (int32_t*)(b + (size_t)off.gfv);
     c->L.base.ggh = (int32_t*)(b + (size_t)off.ggh);
@@ -294,6 +297,19 @@ dmm_status dmm_create(const dmm_config* cfg, void* workspace, size_t bytes, int 
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
         dmm_destroy(c);
         return DMM_E_CUDA;
+    }
+    {   // V half-step tensor maps of every frame (tmap.cu)
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaError_t e = cudaSuccess;
+        for (int f = 0; f < cfg->batch && e == cudaSuccess; ++f) {
+            dmm::FramePtrs P = dmm::frame_ptrs(c->L, f);
+            e = dmm::build_vmaps(P.fv, P.D, cfg->width, cfg->height, c->KP, P.tmap);
+        }
+        if (prev >= 0) cudaSetDevice(prev);
+        c->vtma = e == cudaSuccess;   // else the V kernels stage one bulk copy per node
+        cudaGetLastError();
     }
     if (dmm::gen_mode(cfg)) {
         // edge-weight table (reading R30), computed on the host in double as

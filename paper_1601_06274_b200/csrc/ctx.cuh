@@ -26,6 +26,7 @@ struct ShardState {
     uint32_t* codes_l = nullptr;
     uint32_t* codes_r = nullptr;
     long long* bounds = nullptr;      // [2*max_iters] then energy: one all-reduce
+    int vtma = 0;                     // V band tensor maps encoded
 };
 
 // The captured CUDA graph of one refinement warp (refine.cu), cached per
@@ -54,6 +55,7 @@ struct dmm_ctx {
     int stop_after_h;     // debug: dmm_solve runs only the first H half-step
     int pair_ok;          // configuration passes pair_range_ok
     int use_pair;         // DMM_TUNE_PAIR (default 1): packed chain-pair kernels when pair_ok
+    int vtma = 0;         // the frames' V tensor maps are encoded (tmap.cu)
     struct Rec { int cls; cudaEvent_t a, b; };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;

@@ -51,6 +51,10 @@ struct FramePtrs {
     int32_t* ggh;        // D*2^F + g_    int32 [H][W][KP]
     uint8_t* gom_h;      // edge weights of horizontal edges [H][W]
     uint8_t* gom_v;      // edge weights of vertical edges [H][W], then the 256-entry weight table
+    // 2-D TMA tensor maps (CUtensorMap, 128 B each) of the V half-step's
+    // record / cost arrays (tmap.cu): [0] fv, 16-row boxes (root ring), [1] fv,
+    // 8-row boxes (level ring), [2] fv, 12-row boxes (leaf), [3] D, 12-row boxes
+    uint8_t* tmap;
 };
 
 // Per-frame pointers are base + frame * stride (bytes).
@@ -85,6 +89,7 @@ __host__ __device__ inline FramePtrs frame_ptrs(const Layout& L, int f) {
     p.ggh = (int32_t*)((char*)p.ggh + o);
     p.gom_h += o;
     p.gom_v += o;
+    p.tmap += o;
     return p;
 }
 
@@ -103,6 +108,7 @@ struct PassArgs {
     // (p - segx[s]) for the segment s containing p; nseg <= 1: row-major.
     int nseg;
     const int* segx;  // device [nseg + 1]
+    int vtma;         // V passes stage chunks with the frame's 2-D tensor maps (FramePtrs::tmap)
 };
 
 // kernels (launchers in the .cu files)
@@ -131,6 +137,11 @@ int hm2_launches_per_pass(const PassArgs& a, int vertical);
 bool flow_k_ok(int K);
 void launch_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int K, int KP, int u1_min, int u2_min,
                        int oob, uint8_t* D1, uint8_t* D2, cudaStream_t s);
+// Encode the V tensor maps of one frame (tmap.cu) into dev (4 x 128 B):
+// records `fv` [H][W] of rec bytes, cost volume D [H][W][KP]; box rows 16 / 8 /
+// 12 / 12.  Returns cudaSuccess or the error of the encode / copy.
+constexpr int kTmapBytes = 4 * 128;
+cudaError_t build_vmaps(uint8_t* fv, uint8_t* D, int W, int H, int KP, uint8_t* dev);
 void launch_energy(const Layout& L, int frame0, int nframes, int w_h, int w_v, int T, int fbits,
                    const uint8_t* labels, int32_t* bad, cudaStream_t s);
 void launch_unpad_u8(const uint8_t* src, uint8_t* dst, long long cells, int K, int KP, cudaStream_t s);

@@ -99,7 +99,7 @@ struct Pass {
         n = VERT ? a.L.H : a.L.W;
         nch = VERT ? a.L.W : a.L.H;
         fbits = a.fbits; ws = a.ws; wsT = a.wsT;
-        nseg = a.nseg; segx = a.segx;
+        nseg = a.nseg; segx = a.segx; vtma = a.vtma;
         dk.init(ws, wsT, K, lane);
     }
     __device__ __forceinline__ void set_pair(int pc) {
@@ -109,6 +109,7 @@ struct Pass {
     }
     int nseg;
     const int* segx;
+    int vtma;
     __device__ __forceinline__ int q_of(int c, int p) const { return VERT ? p * W + c : c * W + p; }
     // record index of (chain c, position p) in the records the pass writes
     // (and, unless FIRST, reads): row-major, or column segments for H records
@@ -188,9 +189,12 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
         const int cnt = r_left < kCH ? r_left : kCH;
         const unsigned sbase = ring + slot * slotB;
         const unsigned bar = mbar + 8 * slot;
-        const unsigned long long rev = (!VERT && r_dir < 0) ? 0x80ull : 0ull;
+        // every run is staged in ascending node order; a backward run is read
+        // back to front (the rev bit)
+        const unsigned long long rev = r_dir < 0 ? 0x80ull : 0ull;
         clen = (clen & ~(0xffull << (8 * slot))) | (((unsigned long long)cnt | rev) << (8 * slot));
-        if (this->lane == 0) mbar_expect_tx_s(bar, (unsigned)(2 * cnt * SREC));
+        const bool box = VERT && this->vtma;   // V: one 2-D tensor box of kCH node rows
+        if (this->lane == 0) mbar_expect_tx_s(bar, (unsigned)(2 * (box ? kCH : cnt) * SREC));
         __syncwarp();
         fence_proxy_async();
         __syncwarp();
@@ -206,14 +210,23 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
                            this->src + this->srcq(c, p) * SREC, nn * SREC, bar);
             }
         } else {
-            const int k = this->lane & 15;
-            if (k < cnt) {
-                const int p = r_start + r_dir * k;
-                const size_t q = (size_t)this->qA(p);
-                if (this->hasB) {      // A and B adjacent in HBM
-                    if (this->lane < 16) tma_load_s(sbase + k * kStride, this->src + q * SREC, 2 * SREC, bar);
-                } else {
-                    tma_load_s(sbase + k * kStride + (this->lane < 16 ? 0 : SREC), this->src + q * SREC, SREC, bar);
+            const int first = r_dir > 0 ? r_start : r_start - cnt + 1;
+            if (box) {
+                // rows first .. first + kCH - 1, bytes [cA*REC, cA*REC + 2*REC) of each
+                // (rows past the run or the image are staged / zero-filled and unused)
+                if (this->lane == 0)
+                    tma_load_2d(sbase, this->P.tmap + 128 * (kCH == kRootCH ? 0 : 1), this->cA * (SREC / 8), first, bar);
+            } else {
+                const int k = this->lane & 15;
+                if (k < cnt) {
+                    const int p = first + k;
+                    const size_t q = (size_t)this->qA(p);
+                    if (this->hasB) {      // A and B adjacent in HBM
+                        if (this->lane < 16) tma_load_s(sbase + k * kStride, this->src + q * SREC, 2 * SREC, bar);
+                    } else {
+                        tma_load_s(sbase + k * kStride + (this->lane < 16 ? 0 : SREC), this->src + q * SREC, SREC,
+                                   bar);
+                    }
                 }
             }
         }
@@ -266,7 +279,7 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
     template <int DIR>
     __device__ __forceinline__ void run_pass(int first, int nsteps, MP<LPL>& phi) {
         if (nsteps < 1) return;
-        constexpr bool REV = !VERT && DIR < 0;
+        constexpr bool REV = DIR < 0;      // runs are staged in ascending node order
         const int len0 = nsteps + 1;
         int kk = DIR > 0 ? (31 - __clz(len0)) - 1 : 31 - __clz(len0 - 1);
         int target = DIR > 0 ? (len0 >> kk) : (((len0 - 1) >> kk) + 1);
@@ -572,7 +585,8 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
         int lo0, hi0;
         task_bounds(n, lstar, b & (nbl - 1), lo0, hi0);
         const int m = hi0 - lo0 + 1;
-        const unsigned bytes = 2 * m * SREC + (FIRST ? 0 : 2 * m * KP);
+        const bool box = VERT && h.vtma;          // V: two 2-D tensor boxes of kCMax rows (records, D)
+        const unsigned bytes = box ? 2 * kCMax * (SREC + KP) : 2 * m * SREC + (FIRST ? 0 : 2 * m * KP);
         bulk_wait_read();    // the previous block's output bulk stores have read the staging slots
         __syncwarp();
         if (lane == 0) mbar_expect_tx_s(bar, bytes);
@@ -590,6 +604,9 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
             }
             if (!FIRST && lane == 2) tma_load_s(sD, h.P.D + qa * KP, m * KP, bar);
             if (!FIRST && lane == 3) tma_load_s(sD + kOffD, h.P.D + qb * KP, m * KP, bar);
+        } else if (box) {
+            if (lane == 0) tma_load_2d(sF, h.P.tmap + 256, h.cA * (SREC / 8), lo0, bar);
+            if (lane == 1) tma_load_2d(sD, h.P.tmap + 384, h.cA * (KP / 8), lo0, bar);
         } else {
             const int k = lane & 15;
             if (k < m) {

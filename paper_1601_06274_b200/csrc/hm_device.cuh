@@ -244,6 +244,15 @@ __device__ __forceinline__ void tma_load(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+// 2-D tensor TMA: box at (x, y) of the tensor map at generic address tmap
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const void* tmap, int x, int y, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(tmap), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
 // ---- TMA bulk stores shared -> global (cp.async.bulk ... bulk_group)
 __device__ __forceinline__ void tma_store_s(void* dst, unsigned src, unsigned bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)

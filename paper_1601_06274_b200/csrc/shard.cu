@@ -93,7 +93,7 @@ struct ShardOff {
     size_t img_l, img_r, codes_l, codes_r;
     size_t Dh, fhh, fvh, Dv, fvv, fhv;
     size_t fwd, bwd, fwdo, bwdo;
-    size_t labels_v, labels_full, lab_gather, bounds, flag, segx;
+    size_t labels_v, labels_full, lab_gather, bounds, flag, segx, tmap;
     size_t total;
     int r0, r1, c0, c1;
 };
@@ -136,6 +136,7 @@ ShardOff shard_offsets(const dmm_config* c, int rank, int world) {
     o.bounds = take(8 * (2 * (size_t)c->max_iters + 1));   // bound history, then the energy
     o.flag = take(8);
     o.segx = take(4 * ((size_t)world + 1));
+    o.tmap = take(dmm::kTmapBytes);
     o.total = p;
     return o;
 }
@@ -457,6 +458,11 @@ dmm_status dmm_shard(dmm_ctx* ctx, const uint8_t* id, int rank, int world, int m
         sh.Lv.base.D = (uint8_t*)(b + o.Dv); sh.Lv.base.fv = (uint8_t*)(b + o.fvv); sh.Lv.base.fh = (uint8_t*)(b + o.fhv);
         sh.Lv.frame_bytes = 0;
         sh.Lv.W = o.c1 - o.c0; sh.Lv.H = c.height; sh.Lv.K = ctx->K; sh.Lv.KP = ctx->KP;
+        sh.Lv.base.tmap = (uint8_t*)(b + o.tmap);
+        sh.Lh.base.tmap = nullptr;
+        sh.vtma = dmm::build_vmaps(sh.Lv.base.fv, sh.Lv.base.D, sh.Lv.W, sh.Lv.H, ctx->KP, sh.Lv.base.tmap) ==
+                  cudaSuccess;
+        cudaGetLastError();
         if (cudaMemcpy(sh.segx, sh.cb.data(), 4 * (world + 1), cudaMemcpyHostToDevice) != cudaSuccess) {
             ctx->err = "segment table upload failed";
             return DMM_E_CUDA;
