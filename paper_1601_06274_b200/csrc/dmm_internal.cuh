@@ -53,7 +53,7 @@ struct FramePtrs {
     uint8_t* gom_v;      // edge weights of vertical edges [H][W], then the 256-entry weight table
     // 2-D TMA tensor maps (CUtensorMap, 128 B each) of the V half-step's
     // record / cost arrays (tmap.cu): [0] fv, 16-row boxes (root ring), [1] fv,
-    // 8-row boxes (level ring), [2] fv, 12-row boxes (leaf), [3] D, 12-row boxes
+    // 8-row boxes (level ring), [2] fv, kLeafMax-row boxes (leaf), [3] D, kLeafMax-row boxes
     uint8_t* tmap;
 };
 
@@ -137,6 +137,13 @@ int hm2_launches_per_pass(const PassArgs& a, int vertical);
 bool flow_k_ok(int K);
 void launch_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int K, int KP, int u1_min, int u2_min,
                        int oob, uint8_t* D1, uint8_t* D2, cudaStream_t s);
+// Longest leaf block of the packed pair kernels (nodes); the V tensor maps'
+// leaf boxes have this many rows.  Overridable for experiments.
+#ifndef DMM_CMAX
+#define DMM_CMAX 12
+#endif
+constexpr int kLeafMax = DMM_CMAX;
+
 // Encode the V tensor maps of one frame (tmap.cu) into dev (4 x 128 B):
 // records `fv` [H][W] of rec bytes, cost volume D [H][W][KP]; box rows 16 / 8 /
 // 12 / 12.  Returns cudaSuccess or the error of the encode / copy.

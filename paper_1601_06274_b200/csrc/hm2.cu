@@ -10,7 +10,7 @@ template <int LPL, bool PAD>
 void launch_win(const PassArgs& a, int vertical, int nframes, cudaStream_t s);
 
 namespace {
-constexpr int kCMax = 12;    // longest leaf block (nodes), as hm2_impl.cuh
+constexpr int kCMax = kLeafMax;    // longest leaf block (nodes), as hm2_impl.cuh
 
 int leaf_level(int n) {
     int l = 0;

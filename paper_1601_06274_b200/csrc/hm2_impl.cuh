@@ -19,9 +19,10 @@
 namespace dmm {
 namespace p2 {
 
-constexpr int kCMax = 12;    // longest leaf block (nodes); < 16 (4-bit piece starts)
-constexpr int kDepth = 2;    // pending right pieces in a leaf block (pieces >= 4 nodes push; 12 -> 6 -> 3)
-static_assert(kCMax <= 15, "leaf stack depth 2");
+constexpr int kCMax = kLeafMax;              // longest leaf block (nodes)
+constexpr int kDepth = kCMax > 12 ? 3 : 2;   // pending right pieces (pieces >= 4 nodes push; 12 -> 6 -> 3)
+constexpr int kFB = kCMax > 15 ? 5 : 4;      // bits per packed piece start / end on the stack
+static_assert(kCMax <= 24 && kDepth * kFB <= 32, "leaf stack");
 // Tuning constants (overridable with -D for experiments; the defaults are the measured best)
 #ifndef DMM_NWG
 #define DMM_NWG 2
@@ -687,8 +688,8 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
                 small(lo, hi, L, R);
                 if (sp == 0) break;
                 --sp;
-                lo = (int)((stkJ >> (4 * sp)) & 0xfu);
-                hi = (int)((stkH >> (4 * sp)) & 0xfu);
+                lo = (int)((stkJ >> (kFB * sp)) & ((1u << kFB) - 1));
+                hi = (int)((stkH >> (kFB * sp)) & ((1u << kFB) - 1));
                 __syncwarp();
                 ld_mp_s<LPL>(stk + (2 * sp) * SMP, lane, L);
                 ld_mp_s<LPL>(stk + (2 * sp + 1) * SMP, lane, R);
@@ -742,8 +743,8 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
             handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.dk);
             // children A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R), both >= 2
             // nodes: push B, continue with A
-            stkJ = (stkJ & ~(0xfu << (4 * sp))) | ((unsigned)j << (4 * sp));
-            stkH = (stkH & ~(0xfu << (4 * sp))) | ((unsigned)hi << (4 * sp));
+            stkJ = (stkJ & ~(((1u << kFB) - 1) << (kFB * sp))) | ((unsigned)j << (kFB * sp));
+            stkH = (stkH & ~(((1u << kFB) - 1) << (kFB * sp))) | ((unsigned)hi << (kFB * sp));
             __syncwarp();
             st_mp_s<LPL>(stk + (2 * sp) * SMP, lane, pl);
             st_mp_s<LPL>(stk + (2 * sp + 1) * SMP, lane, R);

@@ -48,8 +48,8 @@ cudaError_t build_vmaps(uint8_t* fv, uint8_t* D, int W, int H, int KP, uint8_t* 
     alignas(64) CUtensorMap m[4];
     static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap is 128 bytes");
     const int rec = rec_bytes(KP);
-    if (!encode(&m[0], fv, W, H, rec, 16) || !encode(&m[1], fv, W, H, rec, 8) || !encode(&m[2], fv, W, H, rec, 12) ||
-        !encode(&m[3], D, W, H, KP, 12))
+    if (!encode(&m[0], fv, W, H, rec, 16) || !encode(&m[1], fv, W, H, rec, 8) ||
+        !encode(&m[2], fv, W, H, rec, kLeafMax) || !encode(&m[3], D, W, H, KP, kLeafMax))
         return cudaErrorInvalidValue;
     return cudaMemcpy(dev, m, sizeof(m), cudaMemcpyHostToDevice);
 }
