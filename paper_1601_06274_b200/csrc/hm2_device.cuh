@@ -54,10 +54,18 @@ __device__ __forceinline__ unsigned op3_2(unsigned a, unsigned b, unsigned c) {
 template <int LPL>
 struct DtK {
     int ws, wsT, K, lane;
+    int ksd;                          // Kogge-Stone path: last round distance needed (see dtrans2)
     unsigned wsP, capP;               // pk(ws), pk(wsT)
     unsigned aL[LPL], aR[LPL];        // per label e: left (e+1)*ws, right (LPL-e)*ws
-    __device__ __forceinline__ void init(int ws_, int wsT_, int K_, int lane_) {
+    __device__ __forceinline__ void init(int ws_, int wsT_, int K_, int lane_, int T_) {
         ws = ws_; wsT = wsT_; K = K_; lane = lane_;
+        // labels of the lane j lanes away are >= (j-1)*LPL + 1 labels apart;
+        // candidates at distance >= T are beaten by the truncation cap, so only
+        // lanes j <= (T-2)/LPL + 1 matter: the scan may stop at the first round
+        // distance d with 2d >= that (the envelope then spans 2d lanes)
+        const int jmax = T_ >= 2 ? (T_ - 2) / LPL + 1 : 1;
+        ksd = 1;
+        while (2 * ksd < jmax && ksd < 16) ksd <<= 1;
         const int cl = wsT + 1;
         const int w1 = min(ws, cl);
         wsP = pk(w1, w1);
@@ -124,6 +132,7 @@ __device__ __forceinline__ unsigned dtrans2(unsigned (&x)[LPL], const DtK<LPL>& 
             const unsigned tb = __shfl_down_sync(kFull, cb, d);
             if (lane >= d) cf = addop2<MAX>(tf, stP, cf);
             if (lane + d < 32) cb = addop2<MAX>(tb, stP, cb);
+            if (d >= k.ksd) break;        // farther lanes only hold candidates above the cap
         }
         inf = __shfl_up_sync(kFull, cf, 1);
         inb = __shfl_down_sync(kFull, cb, 1);

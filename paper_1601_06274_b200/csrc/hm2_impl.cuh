@@ -101,7 +101,7 @@ struct Pass {
         nch = VERT ? a.L.W : a.L.H;
         fbits = a.fbits; ws = a.ws; wsT = a.wsT;
         nseg = a.nseg; segx = a.segx; vtma = a.vtma;
-        dk.init(ws, wsT, K, lane);
+        dk.init(ws, wsT, K, lane, a.T);
     }
     __device__ __forceinline__ void set_pair(int pc) {
         cA = 2 * pc;
