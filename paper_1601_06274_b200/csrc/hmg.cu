@@ -104,20 +104,23 @@ struct GenPass {
         __syncwarp();
         const long long wo = (long long)a.w * omw;
         const int cap = m + (int)((wo * genR(a, a.dc)) >> 4);
+        int best[LPL];
 #pragma unroll
-        for (int e = 0; e < LPL; ++e) {
-            const int b = lane * LPL + e;
-            int best = cap;
-            if (b < a.K) {
-                best = min(best, x[e]);
-                for (int d = 1; d < a.dc; ++d) {
-                    const int v = (int)((wo * genR(a, d)) >> 4);
-                    if (b - d >= 0) best = min(best, sx[b - d] + v);
-                    if (b + d < a.K) best = min(best, sx[b + d] + v);
-                }
+        for (int e = 0; e < LPL; ++e) best[e] = min(cap, x[e]);
+        // distance d < dc (beyond, V = its cap value): V(d) computed once per
+        // distance (warp-uniform), the lane's LPL labels read their two
+        // neighbours at distance d from the staged row
+        for (int d = 1; d < a.dc; ++d) {
+            const int v = (int)((wo * genR(a, d)) >> 4);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) {
+                const int b = lane * LPL + e;
+                if (b - d >= 0) best[e] = min(best[e], sx[b - d] + v);
+                if (b + d < a.K) best[e] = min(best[e], sx[b + d] + v);
             }
-            x[e] = best;
         }
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) x[e] = lane * LPL + e < a.K ? best[e] : cap;
         __syncwarp();
     }
 };
@@ -146,17 +149,27 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
             g.ld(a.Lb, lo, pl);
             g.ld(a.Rb, hi, pr);
         }
+        // the two passes, the next node's costs and edge weight loaded one step ahead
+        int Fn[LPL], omn = 16;
+        if (lo < i) { g.ldF(lo, Fn); omn = g.om(lo); }
         for (int p = lo; p < i; ++p) {               // phi into i from the left (edge p into p+1)
-            g.ldF(p, F);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) F[e] = Fn[e];
+            const int om = omn;
+            if (p + 1 < i) { g.ldF(p + 1, Fn); omn = g.om(p + 1); }
 #pragma unroll
             for (int e = 0; e < LPL; ++e) pl[e] += F[e];
-            g.msg(pl, g.om(p));
+            g.msg(pl, om);
         }
+        if (hi > j) { g.ldF(hi, Fn); omn = g.om(hi - 1); }
         for (int p = hi; p > j; --p) {               // phi into j from the right (edge p-1 into p-1)
-            g.ldF(p, F);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) F[e] = Fn[e];
+            const int om = omn;
+            if (p - 1 > j) { g.ldF(p - 1, Fn); omn = g.om(p - 2); }
 #pragma unroll
             for (int e = 0; e < LPL; ++e) pr[e] += F[e];
-            g.msg(pr, g.om(p - 1));
+            g.msg(pr, om);
         }
         // Handshake (Alg.5, literal three Msg; readings R9, R10)
         const int omij = g.om(i);
