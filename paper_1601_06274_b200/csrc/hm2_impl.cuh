@@ -453,6 +453,117 @@ __global__ void __launch_bounds__(NW * 32, kLevMinCTAs) hm2_level_kernel(PassArg
     pdl_trigger_late();
 }
 
+// ======================================================== last level kernel
+// The level just above the leaves (l* - 1): pieces of <= 2 kCMax nodes, so a
+// task's pass (<= kCMax steps) and its Handshake pair fit one staging area of
+// kLastRows node pairs, filled by one mbarrier phase (H: one bulk copy per
+// chain; V: one 16-row tensor box) -- no ring, no chunk bookkeeping, no
+// nested spine targets: the only spine message the leaves need from this
+// pass is the one into their own first split (the leaf reuses it, "keep"),
+// stored at its node; the Handshake outputs go to fwd[i+1] / bwd[i] as in the
+// generic level kernel.  Same results (the same Msg sequence).
+constexpr int kLastRows = 16;
+static_assert(kLastRows >= kCMax + 2, "a last-level task stages its pass + Handshake nodes");
+
+template <int LPL, bool VERT, bool PAD, int WIN, bool FIRST, int NW>
+__global__ void __launch_bounds__(NW * 32, kLevMinCTAs) hm2_last_kernel(PassArgs a, int lev, int ntasks) {
+    extern __shared__ __align__(128) char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    using PS = Pass<LPL, VERT, PAD, WIN, FIRST>;
+    constexpr int SREC = PS::SREC;
+    constexpr int kStride = VERT ? 2 * SREC : SREC, kOffB = VERT ? SREC : kLastRows * SREC;
+    constexpr int kBytes = align_up(2 * kLastRows * SREC + 8, 128);
+    char* wsm = smem + warp * kBytes;
+    const unsigned sbase = smem_addr(wsm);
+    const unsigned bar = sbase + 2 * kLastRows * SREC;
+    if (lane == 0) { mbar_init(reinterpret_cast<uint64_t*>(wsm + 2 * kLastRows * SREC), 1); fence_mbar_init(); }
+    __syncwarp();
+    unsigned phase = 0;
+    PS h;
+    h.init(a, lane);
+    const int n = h.n;
+    bool waited = false;
+#pragma unroll 1
+    for (int t = blockIdx.x * NW + warp; t < ntasks; t += gridDim.x * NW) {
+        h.set_pair(t >> lev);
+        const int s = t & ((1 << lev) - 1);
+        int lo, hi;
+        task_bounds(n, lev, s, lo, hi);
+        const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
+        const bool left = !(s & 1);
+        const int s0 = left ? ii : lo, s1 = left ? hi : j;     // staged nodes, ascending
+        const int cnt = s1 - s0 + 1;
+        const bool box = VERT && h.vtma;
+        if (lane == 0) mbar_expect_tx_s(bar, (unsigned)(2 * (box ? kLastRows : cnt) * SREC));
+        __syncwarp();
+        fence_proxy_async();
+        __syncwarp();
+        if constexpr (!VERT) {
+            const int n1 = h.run1(s0, cnt, !FIRST);
+            if (lane < 2 || (lane < 4 && n1 < cnt)) {
+                const int c = (lane & 1) ? h.cB : h.cA;
+                const int p = lane < 2 ? s0 : s0 + n1;
+                tma_load_s(sbase + (lane & 1) * kOffB + (lane < 2 ? 0 : n1 * SREC), h.src + h.srcq(c, p) * SREC,
+                           (lane < 2 ? n1 : cnt - n1) * SREC, bar);
+            }
+        } else if (box) {
+            if (lane == 0) tma_load_2d(sbase, h.P.tmap, h.cA * (SREC / 8), s0, bar);
+        } else if (lane < cnt) {
+            const size_t q = (size_t)h.qA(s0 + lane);
+            if (h.hasB) tma_load_s(sbase + lane * kStride, h.src + q * SREC, 2 * SREC, bar);
+            else tma_load_s(sbase + lane * kStride, h.src + q * SREC, SREC, bar);
+        }
+        if (!waited) { pdl_wait(); waited = true; }
+        MP<LPL> bnd, spn;
+        if (left) { h.ld_spine(false, hi, bnd); h.ld_spine(true, ii, spn); }
+        else { h.ld_spine(true, lo, bnd); h.ld_spine(false, j, spn); }
+        mbar_wait_s(bar, phase);
+        __syncwarp();
+        phase ^= 1u;
+        auto slot = [&](int p) { return sbase + (p - s0) * kStride; };
+        // the pass: left piece backward from hi into j, right piece forward from lo into i
+        const int dir = left ? -1 : 1;
+        const int p0 = left ? hi : lo, steps = left ? hi - j : ii - lo;
+        // the leaf's first-split message: right child [j, hi] of a left piece needs
+        // the one into its split + 1 from the right; left child [lo, ii] of a right
+        // piece the one into its split from the left (only for children of >= 4 nodes)
+        const int lr = hi - j + 1, ll = ii - lo + 1;
+        const int tgt = left ? (lr >= 4 ? j + lr / 2 : -1) : (ll >= 4 ? lo + ll / 2 - 1 : -1);
+        unsigned v[LPL];
+        int ba, bb;
+        if (steps > 0) h.dec(slot(p0), slot(p0) + kOffB, v, ba, bb);
+#pragma unroll 1
+        for (int k = 0; k < steps; ++k) {
+            const int p = p0 + dir * k;
+            unsigned vn[LPL];
+            int ban = 0, bbn = 0;
+            const int pn = k + 1 < steps ? p + dir : p;    // in-bounds dummy on the last step
+            h.dec(slot(pn), slot(pn) + kOffB, vn, ban, bbn);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) bnd.m[e] += v[e];
+            bnd.a += ba; bnd.b += bb;
+            h.msg_(bnd.m, bnd.a, bnd.b);                      // message into p + dir
+            if (p + dir == tgt) h.st_spine(!left, tgt, bnd);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) v[e] = vn[e];
+            ba = ban; bb = bbn;
+        }
+        // Handshake over (ii, j)
+        unsigned vi[LPL], vj[LPL];
+        int bia, bib, bja, bjb;
+        h.dec(slot(ii), slot(ii) + kOffB, vi, bia, bib);
+        h.dec(slot(j), slot(j) + kOffB, vj, bja, bjb);
+        MP<LPL>& pl = left ? spn : bnd;
+        MP<LPL>& pr = left ? bnd : spn;
+        handshake2<LPL, PAD, WIN>(vi, bia, bib, vj, bja, bjb, pl, pr, h.dk);
+        h.st_spine(true, ii + 1, pl);
+        h.st_spine(false, ii, pr);
+        __syncwarp();     // the staging area is refilled by the next task
+    }
+    if (!waited) { pdl_wait(); }
+    pdl_trigger_late();
+}
+
 // ============================================================== leaf kernel
 struct LeafShared {     // per-warp shared memory (bytes)
     int F, D, O, stack, mbar, total;
@@ -806,8 +917,12 @@ static void launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, 
 // queried once per device: host API calls between the ~8 launches of a
 // half-step would otherwise starve the GPU.
 struct LaunchCache {
-    int dev = -1, sms = 148, lev_cap = 148, leaf_cap = 148;
+    int dev = -1, sms = 148, lev_cap = 148, leaf_cap = 148, last_cap = 148;
 };
+#ifndef DMM_USE_LAST
+#define DMM_USE_LAST 1
+#endif
+constexpr bool kUseLast = DMM_USE_LAST;
 
 template <int LPL, bool PAD, int WIN, bool FIRST, bool VERT>
 static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
@@ -823,6 +938,8 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
     auto rk = hm2_root_kernel<LPL, VERT, PAD, WIN, FIRST>;
     auto lk = hm2_level_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
     auto kern = hm2_leaf_kernel<LPL, VERT, PAD, WIN, FIRST>;
+    auto lastk = hm2_last_kernel<LPL, VERT, PAD, WIN, FIRST, kNWG>;
+    const int rl = align_up(2 * kLastRows * (FIRST ? KP : rec_bytes(KP)) + 8, 128);
     static LaunchCache lc;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -831,6 +948,10 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
         cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * rr);
         cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNWG * rs);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(lastk, cudaFuncAttributeMaxDynamicSharedMemorySize, kNWG * rl);
+        int per_sm_last = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_last, lastk, kNWG * 32, kNWG * rl);
+        lc.last_cap = lc.sms * (per_sm_last > 0 ? per_sm_last : 1);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lk, kNWG * 32, kNWG * rs);
         lc.lev_cap = lc.sms * (per_sm > 0 ? per_sm : 1);
@@ -843,6 +964,12 @@ static void launch_cfg(const PassArgs& a, int nframes, cudaStream_t s) {
         launch_pdl(true, rk, dim3(units, nframes), 64, 2 * rr, s, a);
         for (int lev = 1; lev < lstar; ++lev) {
             const int ntasks = units << lev;
+            if (lev == lstar - 1 && kUseLast) {      // pieces of <= 2 kCMax nodes: the ring-free kernel
+                int grid = (ntasks + kNWG - 1) / kNWG;
+                if (grid > lc.last_cap) grid = lc.last_cap;
+                launch_pdl(true, lastk, dim3(grid, nframes), kNWG * 32, kNWG * rl, s, a, lev, ntasks);
+                continue;
+            }
             int grid = (ntasks + kNWG - 1) / kNWG;
             if (grid > lc.lev_cap) grid = lc.lev_cap;
             launch_pdl(true, lk, dim3(grid, nframes), kNWG * 32, kNWG * rs, s, a, lev, ntasks);
