@@ -155,3 +155,116 @@ def refine(D, labels, w_h: float, w_v: float, eps: float = 1.0, delta: float = 1
             pv = prox_conj(pv + sigma * bv, w_v, eps, delta, sigma)
             u = u_new
     return u, energy(D, u, w_h, w_v, eps, delta, C)
+
+
+# ===================================================== optical flow (Sec. 3.2)
+# The continuous refinement of a flow field u = (u1, u2): the same
+# regulariser on each component (Eq. regularizer-form sums r over k = 1, 2,
+# P:134-136), the data term approximated around u0 by the quadratic of Eq. 19
+# with finite-difference gradient L and Hessian Q (step h), then
+# the prox of Eq. 20.  Readings (R34-R36):
+#   R34 the Hessian is diagonal (second differences along each component; the
+#       PSD part of a diagonal matrix is max(Q_kk, 0)), which is what makes
+#       Eq. 20's componentwise prox exact; Eq. 20's denominator "1 + tau L^k"
+#       is read as 1 + tau Q_kk (the prox of the quadratic).
+#   R35 D(u) at a real displacement: bilinear interpolation of the census
+#       Hamming costs at the four surrounding integer displacements (out-of-
+#       image displacements cost oob, as in the discrete stage, R23).
+#   R36 L^k = (D(u0 + h e_k) - D(u0 - h e_k)) / (2h), Q_kk = (D(u0 + h e_k) -
+#       2 D(u0) + D(u0 - h e_k)) / h^2 (central differences), h = 1.
+
+def _popc32(x):
+    x = x.astype(np.uint32)
+    x = x - ((x >> 1) & 0x55555555)
+    x = (x & 0x33333333) + ((x >> 2) & 0x33333333)
+    x = (x + (x >> 4)) & 0x0F0F0F0F
+    return ((x * 0x01010101) & 0xFFFFFFFF) >> 24
+
+
+def flow_cost_int(c1, c2, a, b, oob: int = 12):
+    """D(x, y; a, b) = popcount(c1(x,y) ^ c2(x+a, y+b)) at integer displacements
+    (arrays a, b of shape [H][W]), oob outside the image (Eq. flow-decoupled-costs)."""
+    H, W = c1.shape
+    yy, xx = np.mgrid[0:H, 0:W]
+    xs, ys = xx + a, yy + b
+    ok = (xs >= 0) & (xs < W) & (ys >= 0) & (ys < H)
+    v = _popc32(c1 ^ c2[np.clip(ys, 0, H - 1), np.clip(xs, 0, W - 1)]).astype(np.float64)
+    return np.where(ok, v, float(oob))
+
+
+def flow_cost_bilinear(c1, c2, u1, u2, oob: int = 12):
+    """D at real displacements (reading R35)."""
+    a0 = np.floor(u1)
+    b0 = np.floor(u2)
+    fx = u1 - a0
+    fy = u2 - b0
+    a0 = a0.astype(np.int64)
+    b0 = b0.astype(np.int64)
+    d00 = flow_cost_int(c1, c2, a0, b0, oob)
+    d10 = flow_cost_int(c1, c2, a0 + 1, b0, oob)
+    d01 = flow_cost_int(c1, c2, a0, b0 + 1, oob)
+    d11 = flow_cost_int(c1, c2, a0 + 1, b0 + 1, oob)
+    return ((1.0 - fx) * (1.0 - fy) * d00 + fx * (1.0 - fy) * d10) + ((1.0 - fx) * fy * d01 + fx * fy * d11)
+
+
+def flow_quadratic(c1, c2, u1, u2, h: float, oob: int = 12):
+    """(L1, Q11, L2, Q22) of Eq. 19 around (u1, u2) (readings R34, R36)."""
+    d0 = flow_cost_bilinear(c1, c2, u1, u2, oob)
+    dp1 = flow_cost_bilinear(c1, c2, u1 + h, u2, oob)
+    dm1 = flow_cost_bilinear(c1, c2, u1 - h, u2, oob)
+    dp2 = flow_cost_bilinear(c1, c2, u1, u2 + h, oob)
+    dm2 = flow_cost_bilinear(c1, c2, u1, u2 - h, oob)
+    L1 = (dp1 - dm1) / (2.0 * h)
+    L2 = (dp2 - dm2) / (2.0 * h)
+    Q1 = np.maximum((dp1 - 2.0 * d0 + dm1) / (h * h), 0.0)
+    Q2 = np.maximum((dp2 - 2.0 * d0 + dm2) / (h * h), 0.0)
+    return L1, Q1, L2, Q2
+
+
+def prox_quadratic(uh, u0, L, Q, tau: float, h: float):
+    """Prox of tau * D~ for the quadratic of Eq. 19 per component (Eq. 20 with
+    reading R34), then the clamp to [u0 - h, u0 + h]."""
+    v = (uh + tau * (Q * u0 - L)) / (1.0 + tau * Q)
+    return np.clip(v, u0 - h, u0 + h)
+
+
+def flow_energy(c1, c2, u1, u2, w_h, w_v, eps, delta, C, oob: int = 12):
+    e = flow_cost_bilinear(c1, c2, u1, u2, oob).sum()
+    for u in (u1, u2):
+        ah, av = A(u)
+        e += w_h * r_dc(ah, eps, delta, C).sum() + w_v * r_dc(av, eps, delta, C).sum()
+    return float(e)
+
+
+def flow_refine(c1, c2, u1, u2, w_h: float, w_v: float, eps: float = 1.0, delta: float = 1.0, C: float = 4.0,
+                h: float = 1.0, tau: float = 0.35, sigma: float = 0.35, warps: int = 5, iters: int = 40,
+                oob: int = 12):
+    """Refine an integer flow field (u1, u2) (pixels).  Per warp the quadratic
+    model is rebuilt at the current u; each component then runs the same
+    iterates as the stereo refinement with the quadratic prox (the components
+    couple only through the re-linearisation).  Returns (u1, u2, energy)."""
+    c1 = np.asarray(c1, np.uint32)
+    c2 = np.asarray(c2, np.uint32)
+    H, W = c1.shape
+    us = [np.asarray(u1, np.float64).copy(), np.asarray(u2, np.float64).copy()]
+    st = [dict(ph=np.zeros((H, W - 1)), pv=np.zeros((H - 1, W)), qh=np.zeros((H, W - 1)), qv=np.zeros((H - 1, W)))
+          for _ in range(2)]
+    bp = C + delta - eps * delta
+    for _ in range(warps):
+        L1, Q1, L2, Q2 = flow_quadratic(c1, c2, us[0], us[1], h, oob)
+        for k, (L, Q) in enumerate(((L1, Q1), (L2, Q2))):
+            u = us[k]
+            u0 = u.copy()
+            s = st[k]
+            for _ in range(iters):
+                uh = u - tau * AT(s["ph"] - s["qh"], s["pv"] - s["qv"], (H, W))
+                u_new = prox_quadratic(uh, u0, L, Q, tau, h)
+                ah, av = A(u)
+                s["qh"] = prox_conj(s["qh"] + tau * ah, w_h, 0.0, bp, tau)
+                s["qv"] = prox_conj(s["qv"] + tau * av, w_v, 0.0, bp, tau)
+                bh, bv = A(2.0 * u_new - u)
+                s["ph"] = prox_conj(s["ph"] + sigma * bh, w_h, eps, delta, sigma)
+                s["pv"] = prox_conj(s["pv"] + sigma * bv, w_v, eps, delta, sigma)
+                u = u_new
+            us[k] = u
+    return us[0], us[1], flow_energy(c1, c2, us[0], us[1], w_h, w_v, eps, delta, C, oob)

@@ -109,3 +109,51 @@ def test_refinement_runs_and_interpolates():
     assert np.array_equal(rf.D_interp(D, lab.astype(np.float64)), D[np.arange(H)[:, None], np.arange(W), lab])
     u, e = rf.refine(D, lab, 0.5, 0.5, eps=1.0, delta=1.0, C=4.0)
     assert np.abs(u - true[None, :]).mean() < np.abs(lab - true[None, :]).mean()
+
+
+# ------------------------------------------------------- flow (Sec. 3.2)
+def test_flow_cost_bilinear_at_integers_is_the_census_cost(orc):
+    """D at integer displacements is the census Hamming cost of the discrete
+    stage: the minimum over the vertical window equals oracle_flow_costs' f1."""
+    import datagen
+    i1, i2, _, _ = datagen.flow_pair(40, 24, 8, seed=1)
+    c1, c2 = orc.census(i1), orc.census(i2)
+    f1, f2 = orc.flow_costs(c1, c2, -8, 16, -8, 16)
+    H, W = c1.shape
+    for a in range(-8, 8):
+        best = np.full((H, W), np.inf)
+        for b in range(-8, 8):
+            d = rf.flow_cost_bilinear(c1, c2, np.full((H, W), float(a)), np.full((H, W), float(b)))
+            assert np.array_equal(d, rf.flow_cost_int(c1, c2, np.full((H, W), a), np.full((H, W), b)))
+            best = np.minimum(best, d)
+        assert np.array_equal(best, f1[:, :, a + 8].astype(np.float64))
+
+
+def test_prox_quadratic_by_grid_search():
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        u0, L, Q = rng.uniform(-10, 10), rng.uniform(-20, 20), rng.uniform(0, 30)
+        tau, h = rng.uniform(0.05, 1.0), rng.uniform(0.5, 2.0)
+        uh = u0 + rng.uniform(-5, 5)
+        grid = np.linspace(u0 - h, u0 + h, 20001)
+        obj = tau * (L * (grid - u0) + 0.5 * Q * (grid - u0) ** 2) + 0.5 * (grid - uh) ** 2
+        got = rf.prox_quadratic(np.array([uh]), np.array([u0]), np.array([L]), np.array([Q]), tau, h)[0]
+        assert abs(got - grid[np.argmin(obj)]) < 2e-4
+
+
+def test_flow_refine_zero_regularisation(orc):
+    """w = 0, one warp: each component minimises its own quadratic model on
+    [u0 - h, u0 + h] (closed form of Eq. 19 restricted to the box)."""
+    import datagen
+    i1, i2, g1, g2 = datagen.flow_pair(30, 20, 8, seed=2)
+    c1, c2 = orc.census(i1), orc.census(i2)
+    u1 = np.clip(g1, -7, 7).astype(np.float64)
+    u2 = np.clip(g2, -7, 7).astype(np.float64)
+    r1, r2, _ = rf.flow_refine(c1, c2, u1, u2, 0.0, 0.0, warps=1, iters=400)
+    L1, Q1, L2, Q2 = rf.flow_quadratic(c1, c2, u1, u2, 1.0)
+    for u0, L, Q, r in ((u1, L1, Q1, r1), (u2, L2, Q2, r2)):
+        grid = u0[..., None] + np.linspace(-1, 1, 2001)[None, None, :]
+        obj = L[..., None] * (grid - u0[..., None]) + 0.5 * Q[..., None] * (grid - u0[..., None]) ** 2
+        mn = obj.min(-1)
+        got = L * (r - u0) + 0.5 * Q * (r - u0) ** 2
+        assert np.all(got <= mn + 1e-6)
