@@ -188,6 +188,19 @@ typedef struct dmm_refine_params {
 DMM_API dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* u_out, double* energy,
                               void* stream);
 
+/* Continuous refinement of an optical flow field (NEXT-2; Sec. 3.2
+ * P:449-467): u1 = d_min + labels of frame `frame`, u2 = v_min + labels of
+ * frame `frame + 1` (after dmm_flow_cost_volume + dmm_solve of both layers)
+ * refined with the regulariser of dmm_refine on each component and the data
+ * term approximated by the quadratic of Eq. 19 (central-difference gradient
+ * and diagonal Hessian of the census cost at the current flow, bilinear between
+ * integer displacements; readings R34-R36) with the componentwise prox of
+ * Eq. 20.  float64 on the device; u1_out / u2_out (nullable) device float
+ * [H][W] in pixels; energy (nullable, host) = sum D(u) + R(Au1) + R(Au2),
+ * synchronises `stream` when given. */
+DMM_API dmm_status dmm_flow_refine(dmm_ctx* ctx, int frame, int32_t v_min, const dmm_refine_params* prm,
+                                   float* u1_out, float* u2_out, double* energy, void* stream);
+
 /* Optical flow, discrete stage (NEXT-1; Eq. "flow decoupled costs"
  * P:163-170, Sec. 3.2): census codes of both images into frame
  * `frame`, then the optimistic decoupled costs of the 2-D label window

@@ -28,7 +28,7 @@ EXPORTS = (
     "dmm_set_profiling", "dmm_read_profile", "dmm_set_tuning", "dmm_msg", "dmm_handshake",
     "dmm_buffer_ptr", "dmm_import_cost_volume", "dmm_half_step", "dmm_energy",
     "dmm_cost_volume_frames", "dmm_run_host_frames", "dmm_energy_of",
-    "dmm_flow_cost_volume", "dmm_refine", "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
+    "dmm_flow_cost_volume", "dmm_refine", "dmm_flow_refine", "dmm_nccl_unique_id", "dmm_shard", "dmm_shard_workspace_bytes", "dmm_shard_plan", "dmm_shard_locate",
 )
 SHARD_FRAMES, SHARD_ROWCOL = 0, 1
 LOC_FV_H, LOC_FH_H, LOC_FV_V, LOC_FH_V, LOC_LABEL_V, LOC_BOUNDS = range(6)
@@ -117,6 +117,8 @@ def load_library():
         "dmm_flow_cost_volume": (ctypes.c_int, [P, ctypes.c_int, P, P, i64, i32, P]),
         "dmm_refine": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(DmmRefineParams), P,
                                       ctypes.POINTER(ctypes.c_double), P]),
+        "dmm_flow_refine": (ctypes.c_int, [P, ctypes.c_int, i32, ctypes.POINTER(DmmRefineParams), P, P,
+                                           ctypes.POINTER(ctypes.c_double), P]),
         "dmm_nccl_unique_id": (ctypes.c_int, [P]),
         "dmm_shard": (ctypes.c_int, [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "dmm_shard_workspace_bytes": (ctypes.c_size_t, [C, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
@@ -312,6 +314,21 @@ class Context:
         self._call("dmm_refine", frame, ctypes.byref(prm), ctypes.c_void_p(out.data_ptr()),
                    ctypes.byref(e) if energy else None, _stream_handle(stream, self.device))
         return out, (float(e.value) if energy else None)
+
+    def flow_refine(self, v_min: int, eps: float = 1.0, delta: float = 1.0, C: float | None = None, h: float = 1.0,
+                    tau: float = 0.35, sigma: float = 0.35, warps: int = 5, iters: int = 40, frame: int = 0,
+                    stream=None, energy: bool = True):
+        """Continuous refinement of the flow of layers (frame, frame + 1)
+        (dmm_flow_refine): returns (u1, u2, energy), float32 (H, W) on the device."""
+        import torch
+        prm = DmmRefineParams(eps, delta, float(self.cfg.trunc if C is None else C), h, tau, sigma, warps, iters)
+        u1 = torch.empty((self.H, self.W), dtype=torch.float32, device=self.device)
+        u2 = torch.empty_like(u1)
+        e = ctypes.c_double()
+        self._call("dmm_flow_refine", frame, v_min, ctypes.byref(prm), ctypes.c_void_p(u1.data_ptr()),
+                   ctypes.c_void_p(u2.data_ptr()), ctypes.byref(e) if energy else None,
+                   _stream_handle(stream, self.device))
+        return u1, u2, (float(e.value) if energy else None)
 
     def flow_cost_volume(self, left, right, v_min: int, frame: int = 0, stream=None):
         """Optical flow, discrete stage (dmm_flow_cost_volume): the decoupled

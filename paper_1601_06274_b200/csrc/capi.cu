@@ -398,6 +398,37 @@ dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
     return DMM_OK;
 }
 
+dmm_status dmm_flow_refine(dmm_ctx* ctx, int frame, int32_t v_min, const dmm_refine_params* prm, float* u1_out,
+                           float* u2_out, double* energy, void* stream) {
+    if (!ctx) return DMM_E_ARG;
+    DMM_DEVICE_GUARD(ctx);
+    dmm_status st = frame_ok(ctx, frame, 2);
+    if (st || (st = not_sharded(ctx, "dmm_flow_refine"))) return st;
+    if (!prm || prm->warps < 0 || prm->iters < 0 || prm->iters > 4096 || !(prm->h > 0.0) || !(prm->tau > 0.0) ||
+        !(prm->sigma > 0.0) || !(prm->eps >= 0.0 && prm->eps <= 1.0) || !(prm->delta >= 0.0) || !(prm->C >= 0.0)) {
+        ctx->err = "bad refinement parameters";
+        return DMM_E_ARG;
+    }
+    if (ctx->iters_done[frame] < 1 || ctx->iters_done[frame + 1] < 1) {
+        ctx->err = "flow refine before both layers are solved";
+        return DMM_E_STATE;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    dmm::FramePtrs P = dmm::frame_ptrs(ctx->L, frame);
+    if (energy && (st = cuda_err(ctx, cudaMemsetAsync(P.renergy, 0, 8, s), "memset"))) return st;
+    {
+        Timed t(ctx, 5, s, 0);
+        if ((st = dmm::refine_flow_run(ctx, frame, (double)ctx->cfg.d_min, (double)v_min, prm, u1_out, u2_out,
+                                       energy ? P.renergy : nullptr, s)))
+            return st;
+    }
+    if (energy) {
+        if ((st = cuda_err(ctx, cudaMemcpyAsync(energy, P.renergy, 8, cudaMemcpyDeviceToHost, s), "d2h"))) return st;
+        if ((st = cuda_err(ctx, cudaStreamSynchronize(s), "sync"))) return st;
+    }
+    return DMM_OK;
+}
+
 dmm_status dmm_flow_cost_volume(dmm_ctx* ctx, int frame, const uint8_t* left, const uint8_t* right, int64_t pitch,
                                 int32_t v_min, void* stream) {
     if (!ctx) return DMM_E_ARG;

@@ -60,7 +60,8 @@ struct dmm_ctx {
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
     ShardState sh;
-    RefineGraph rg;
+    RefineGraph rg;       // stereo refinement
+    RefineGraph rgf;      // flow refinement
 };
 
 namespace dmm {
@@ -86,4 +87,6 @@ size_t refine_bytes(int W, int H);
 dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,
                       cudaStream_t s);
 void refine_release(dmm_ctx* ctx);
+dmm_status refine_flow_run(dmm_ctx* ctx, int frame, double u1_min, double u2_min, const dmm_refine_params* prm,
+                           float* out1, float* out2, double* energy_dev, cudaStream_t s);
 }  // namespace dmm

@@ -90,7 +90,10 @@ __global__ void refine_warp_kernel(RefArgs a) {
     arr(a, 4)[i] = s2;
 }
 
-// u+ at pixel j = (jy, jx): prox_{tau D~}(u - tau A^T (p - q)) (R25)
+// u+ at pixel j = (jy, jx): prox_{tau D~}(u - tau A^T (p - q)): the two-slope
+// data term of stereo (R25; slots 3/4 = s1, s2) or, QUAD, the
+// quadratic of flow (Eq. 19/20, R34; slots 3/4 = L, Q)
+template <bool QUAD>
 __device__ __forceinline__ real primal_u(const RefArgs& a, const real* u, const real* ph, const real* pv,
                                          const real* qh, const real* qv, int jx, int jy) {
     const int W = a.W, H = a.H;
@@ -102,7 +105,11 @@ __device__ __forceinline__ real primal_u(const RefArgs& a, const real* u, const 
     if (jy > 0) div -= pv[j - W] - qv[j - W];
     const real uh = u[j] - a.tau * div;
     const real u0 = arr(a, 2)[j], s1 = arr(a, 3)[j], s2 = arr(a, 4)[j];
-    const real v = uh > u0 + a.tau * s2 ? uh - a.tau * s2 : (uh < u0 + a.tau * s1 ? uh - a.tau * s1 : u0);
+    real v;
+    if constexpr (QUAD)
+        v = (uh + a.tau * (s2 * u0 - s1)) / (1.0 + a.tau * s2);
+    else
+        v = uh > u0 + a.tau * s2 ? uh - a.tau * s2 : (uh < u0 + a.tau * s1 ? uh - a.tau * s1 : u0);
     return fmin(fmax(v, u0 - a.h), u0 + a.h);
 }
 
@@ -112,6 +119,7 @@ __device__ __forceinline__ real primal_u(const RefArgs& a, const real* u, const 
 // launch), then q+ (from u) and p+ (from 2u+ - u) of its own edges.  Reads
 // buffer cur, writes buffer 1 - cur (u, q) and p in place (each edge owned by
 // one pixel, read by no other thread of this launch).
+template <bool QUAD>
 __global__ void refine_iter_kernel(RefArgs a, int cur) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
@@ -125,17 +133,17 @@ __global__ void refine_iter_kernel(RefArgs a, int cur) {
     const real* qh = arr(a, b0 + 2);
     const real* qv = arr(a, b0 + 3);
     const real ui = u[i];
-    const real uni = primal_u(a, u, ph, pv, qh, qv, x, y);
+    const real uni = primal_u<QUAD>(a, u, ph, pv, qh, qv, x, y);
     const real bp = a.C + a.delta - a.eps * a.delta;
     const real bi = 2.0 * uni - ui;
     if (x + 1 < W) {
-        const real unr = primal_u(a, u, ph, pv, qh, qv, x + 1, y);
+        const real unr = primal_u<QUAD>(a, u, ph, pv, qh, qv, x + 1, y);
         const real ur = u[i + 1];
         arr(a, b1 + 2)[i] = prox_conj(qh[i] + a.tau * (ui - ur), a.wh, 0.0, bp, a.tau);       // q+ = prox(q + tau A u)
         arr(a, b1)[i] = prox_conj(ph[i] + a.sigma * (bi - (2.0 * unr - ur)), a.wh, a.eps, a.delta, a.sigma);
     }
     if (y + 1 < H) {
-        const real und = primal_u(a, u, ph, pv, qh, qv, x, y + 1);
+        const real und = primal_u<QUAD>(a, u, ph, pv, qh, qv, x, y + 1);
         const real ud = u[i + W];
         arr(a, b1 + 3)[i] = prox_conj(qv[i] + a.tau * (ui - ud), a.wv, 0.0, bp, a.tau);
         arr(a, b1 + 1)[i] = prox_conj(pv[i] + a.sigma * (bi - (2.0 * und - ud)), a.wv, a.eps, a.delta, a.sigma);
@@ -177,12 +185,90 @@ __global__ void refine_out_kernel(RefArgs a, real d_min, float* out, double* ene
     }
 }
 
-}  // namespace
+// ------------------------------------------------------------- optical flow
+// D at a real displacement (reading R35): bilinear over the census Hamming
+// costs of the four surrounding integer displacements (oob outside the image),
+// in the oracle's operation order.
+struct FlowArgs {
+    const uint32_t* c1;
+    const uint32_t* c2;
+    int W, H;
+    real oob;
+};
 
-size_t refine_bytes(int W, int H) { return (size_t)kRefArrays * sizeof(real) * W * H; }
+__device__ __forceinline__ real flow_cost_int(const FlowArgs& f, int x, int y, long long a, long long b) {
+    const long long xs = x + a, ys = y + b;
+    if (xs < 0 || xs >= f.W || ys < 0 || ys >= f.H) return f.oob;
+    return (real)__popc(f.c1[(size_t)y * f.W + x] ^ f.c2[(size_t)ys * f.W + xs]);
+}
 
-dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,
-                      cudaStream_t s) {
+__device__ __forceinline__ real flow_cost_bilinear(const FlowArgs& f, int x, int y, real u1, real u2) {
+    const real a0 = floor(u1), b0 = floor(u2);
+    const real fx = u1 - a0, fy = u2 - b0;
+    const long long ia = (long long)a0, ib = (long long)b0;
+    const real d00 = flow_cost_int(f, x, y, ia, ib), d10 = flow_cost_int(f, x, y, ia + 1, ib);
+    const real d01 = flow_cost_int(f, x, y, ia, ib + 1), d11 = flow_cost_int(f, x, y, ia + 1, ib + 1);
+    return ((1.0 - fx) * (1.0 - fy) * d00 + fx * (1.0 - fy) * d10) + ((1.0 - fx) * fy * d01 + fx * fy * d11);
+}
+
+// the layers' labels -> displacements; duals of both components 0
+__global__ void flow_init_kernel(RefArgs a1, RefArgs a2, real u1_min, real u2_min) {
+    const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
+    if (x >= a1.W || y >= a1.H) return;
+    const size_t i = (size_t)y * a1.W + x;
+    arr(a1, 0)[i] = u1_min + (real)a1.labels[i];
+    arr(a2, 0)[i] = u2_min + (real)a2.labels[i];
+    for (int k = 5; k < kRefArrays; ++k) { arr(a1, k)[i] = 0.0; arr(a2, k)[i] = 0.0; }
+}
+
+// the quadratic model of Eq. 19 at the current (u1, u2) (readings R34, R36):
+// u0 -> slot 2, L -> slot 3, Q (PSD part) -> slot 4 of each component
+__global__ void flow_warp_kernel(RefArgs a1, RefArgs a2, FlowArgs f) {
+    const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
+    if (x >= a1.W || y >= a1.H) return;
+    const size_t i = (size_t)y * a1.W + x;
+    const real u1 = arr(a1, 0)[i], u2 = arr(a2, 0)[i], h = a1.h;
+    const real d0 = flow_cost_bilinear(f, x, y, u1, u2);
+    const real dp1 = flow_cost_bilinear(f, x, y, u1 + h, u2), dm1 = flow_cost_bilinear(f, x, y, u1 - h, u2);
+    const real dp2 = flow_cost_bilinear(f, x, y, u1, u2 + h), dm2 = flow_cost_bilinear(f, x, y, u1, u2 - h);
+    arr(a1, 2)[i] = u1;
+    arr(a1, 3)[i] = (dp1 - dm1) / (2.0 * h);
+    arr(a1, 4)[i] = fmax((dp1 - 2.0 * d0 + dm1) / (h * h), 0.0);
+    arr(a2, 2)[i] = u2;
+    arr(a2, 3)[i] = (dp2 - dm2) / (2.0 * h);
+    arr(a2, 4)[i] = fmax((dp2 - 2.0 * d0 + dm2) / (h * h), 0.0);
+}
+
+__global__ void flow_out_kernel(RefArgs a1, RefArgs a2, FlowArgs f, float* out1, float* out2, double* energy) {
+    const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
+    double e = 0.0;
+    if (x < a1.W && y < a1.H) {
+        const int W = a1.W;
+        const size_t i = (size_t)y * W + x;
+        const real* u1 = arr(a1, 0);
+        const real* u2 = arr(a2, 0);
+        if (out1) out1[i] = (float)u1[i];
+        if (out2) out2[i] = (float)u2[i];
+        e = flow_cost_bilinear(f, x, y, u1[i], u2[i]);
+        const real* us[2] = {u1, u2};
+        for (int k = 0; k < 2; ++k) {
+            if (x + 1 < W) e += a1.wh * r_dc(us[k][i] - us[k][i + 1], a1.eps, a1.delta, a1.C);
+            if (y + 1 < a1.H) e += a1.wv * r_dc(us[k][i] - us[k][i + W], a1.eps, a1.delta, a1.C);
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) e += __shfl_down_sync(0xffffffffu, e, d);
+    __shared__ double part[kRX * kRY / 32];
+    const int t = threadIdx.y * kRX + threadIdx.x;
+    if ((t & 31) == 0) part[t >> 5] = e;
+    __syncthreads();
+    if (t == 0 && energy) {
+        double s = 0.0;
+        for (int k = 0; k < kRX * kRY / 32; ++k) s += part[k];
+        atomicAdd(energy, s);
+    }
+}
+
+RefArgs ref_args(dmm_ctx* ctx, int frame, const dmm_refine_params* prm) {
     FramePtrs P = frame_ptrs(ctx->L, frame);
     RefArgs a;
     a.rf = reinterpret_cast<real*>(P.rf);
@@ -191,6 +277,17 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
     a.W = ctx->L.W; a.H = ctx->L.H; a.K = ctx->K; a.KP = ctx->KP;
     a.wh = (real)ctx->cfg.w_h; a.wv = (real)ctx->cfg.w_v;
     a.eps = prm->eps; a.delta = prm->delta; a.C = prm->C; a.h = prm->h; a.tau = prm->tau; a.sigma = prm->sigma;
+    return a;
+}
+
+}  // namespace
+
+size_t refine_bytes(int W, int H) { return (size_t)kRefArrays * sizeof(real) * W * H; }
+
+dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, float* out, double* energy_dev,
+                      cudaStream_t s) {
+    FramePtrs P = frame_ptrs(ctx->L, frame);
+    RefArgs a = ref_args(ctx, frame, prm);
     const dim3 grid((a.W + kRX - 1) / kRX, (a.H + kRY - 1) / kRY), blk(kRX, kRY);
     refine_init_kernel<<<grid, blk, 0, s>>>(a);
     ++ctx->launches;
@@ -209,7 +306,7 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
         refine_warp_kernel<<<grid, blk, 0, g.cap>>>(a);
         int cur = 0;
         for (int it = 0; it < prm->iters; ++it) {
-            refine_iter_kernel<<<grid, blk, 0, g.cap>>>(a, cur);
+            refine_iter_kernel<false><<<grid, blk, 0, g.cap>>>(a, cur);
             cur ^= 1;
         }
         if (cur) refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a);
@@ -232,11 +329,63 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
     return cuda_status(ctx, cudaGetLastError(), "refine");
 }
 
+
+// Flow refinement (Sec. 3.2): layer frames `frame` (u1) and `frame + 1` (u2)
+// of a flow context; census codes of frame `frame`.
+dmm_status refine_flow_run(dmm_ctx* ctx, int frame, double u1_min, double u2_min, const dmm_refine_params* prm,
+                           float* out1, float* out2, double* energy_dev, cudaStream_t s) {
+    RefArgs a1 = ref_args(ctx, frame, prm), a2 = ref_args(ctx, frame + 1, prm);
+    FramePtrs P = frame_ptrs(ctx->L, frame);
+    FlowArgs f{P.codes_l, P.codes_r, ctx->L.W, ctx->L.H, (real)ctx->oob};
+    const dim3 grid((a1.W + kRX - 1) / kRX, (a1.H + kRY - 1) / kRY), blk(kRX, kRY);
+    flow_init_kernel<<<grid, blk, 0, s>>>(a1, a2, u1_min, u2_min);
+    ++ctx->launches;
+    RefineGraph& g = ctx->rgf;
+    const bool same = g.exec && g.frame == frame && memcmp(&g.prm, prm, sizeof(*prm)) == 0 && g.rf == P.rf;
+    if (!same) {
+        if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
+        if (!g.cap && cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking) != cudaSuccess)
+            return cuda_status(ctx, cudaGetLastError(), "refine capture stream");
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture");
+        flow_warp_kernel<<<grid, blk, 0, g.cap>>>(a1, a2, f);
+        int cur = 0;
+        for (int it = 0; it < prm->iters; ++it) {
+            refine_iter_kernel<true><<<grid, blk, 0, g.cap>>>(a1, cur);
+            refine_iter_kernel<true><<<grid, blk, 0, g.cap>>>(a2, cur);
+            cur ^= 1;
+        }
+        if (cur) {
+            refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a1);
+            refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a2);
+        }
+        e = cudaStreamEndCapture(g.cap, &graph);
+        if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture end");
+        e = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine graph instantiate");
+        g.frame = frame;
+        g.prm = *prm;
+        g.rf = P.rf;
+    }
+    for (int w = 0; w < prm->warps; ++w) {
+        cudaError_t e = cudaGraphLaunch(g.exec, s);
+        if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine graph launch");
+        ctx->launches += 1 + 2 * prm->iters + 2 * (prm->iters & 1);
+    }
+    flow_out_kernel<<<grid, blk, 0, s>>>(a1, a2, f, out1, out2, energy_dev);
+    ++ctx->launches;
+    return cuda_status(ctx, cudaGetLastError(), "flow refine");
+}
+
 void refine_release(dmm_ctx* ctx) {
-    if (ctx->rg.exec) cudaGraphExecDestroy(ctx->rg.exec);
-    if (ctx->rg.cap) cudaStreamDestroy(ctx->rg.cap);
-    ctx->rg.exec = nullptr;
-    ctx->rg.cap = nullptr;
+    for (RefineGraph* g : {&ctx->rg, &ctx->rgf}) {
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        if (g->cap) cudaStreamDestroy(g->cap);
+        g->exec = nullptr;
+        g->cap = nullptr;
+    }
 }
 
 }  // namespace dmm

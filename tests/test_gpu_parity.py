@@ -594,6 +594,58 @@ def test_refine_c2_full_size(orc):
     assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
 
 
+def _flow_refine_case(orc, W, H, K, u1_min, u2_min, prm):
+    from oracle import refine as orf
+    i1, i2, _, _ = datagen.flow_pair(W, H, min(K // 2, 16), seed=W * 7 + H)
+    ctx = _ctx(width=W, height=H, d_min=u1_min, d_max=u1_min + K - 1, batch=2, max_iters=4)
+    ctx.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i2).cuda(), u2_min)
+    ctx.solve(4, frame=0, nframes=2)
+    g1, g2, e = ctx.flow_refine(u2_min, **prm)
+    u1 = u1_min + ctx.labels(0).cpu().numpy().astype(np.float64)
+    u2 = u2_min + ctx.labels(1).cpu().numpy().astype(np.float64)
+    o1, o2, eo = orf.flow_refine(orc.census(i1), orc.census(i2), u1, u2, 3.0, 3.0, **prm)
+    return ctx, (g1, g2, e), (o1, o2, eo)
+
+
+@pytest.mark.parametrize("W,H,K,u1,u2,prm", [
+    (77, 45, 32, -16, -16, dict(C=4.0)),
+    (61, 23, 16, -8, -3, dict(eps=0.5, delta=2.0, C=5.0, warps=3, iters=25)),
+    (40, 70, 48, -20, -30, dict(eps=0.25, delta=1.0, C=3.0, warps=2, iters=7, tau=0.2, sigma=0.5))])
+def test_flow_refine_parity(orc, W, H, K, u1, u2, prm):
+    """dmm_flow_refine (quadratic model of Eq. 19 rebuilt per warp, Eq. 20's
+    prox, float64 without FMA) vs oracle.refine.flow_refine from the same two
+    discrete layers: u1, u2 bit-exact after rounding to float32."""
+    ctx, (g1, g2, e), (o1, o2, eo) = _flow_refine_case(orc, W, H, K, u1, u2, prm)
+    assert np.array_equal(g1.cpu().numpy(), o1.astype(np.float32))
+    assert np.array_equal(g2.cpu().numpy(), o2.astype(np.float32))
+    assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
+    h1, h2, e2 = ctx.flow_refine(u2, **prm)              # replays the cached graph
+    assert torch.equal(g1, h1) and torch.equal(g2, h2) and abs(e2 - e) <= 1e-12 * abs(e)
+
+
+def test_flow_refine_c4_full_size(orc):
+    """configs[3] (C4): 1242x375, 32x32 window, 4 Dual MM iterations per layer,
+    then the continuous refinement (5 warps x 40 iterations)."""
+    c = datagen.CONFIGS["C4"]
+    _, (g1, g2, e), (o1, o2, eo) = _flow_refine_case(orc, c["W"], c["H"], c["K"], -16, -16, dict(C=4.0))
+    assert np.array_equal(g1.cpu().numpy(), o1.astype(np.float32))
+    assert np.array_equal(g2.cpu().numpy(), o2.astype(np.float32))
+    assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
+
+
+def test_flow_refine_state_errors():
+    import paper_1601_06274_b200 as dmm
+    i1 = np.random.default_rng(0).integers(0, 255, (20, 30)).astype(np.uint8)
+    ctx = _ctx(width=30, height=20, d_min=-8, d_max=7, batch=2)
+    ctx.flow_cost_volume(torch.from_numpy(i1).cuda(), torch.from_numpy(i1).cuda(), -8)
+    with pytest.raises(dmm.DmmError):
+        ctx.flow_refine(-8)                              # layers not solved
+    ctx.solve(1, frame=0, nframes=2)
+    with pytest.raises(dmm.DmmError):
+        ctx.flow_refine(-8, tau=0.0)
+    ctx.flow_refine(-8, warps=1, iters=1)
+
+
 # --------------------------------------- NEXT-3 general penalty + edge weights
 def _gen_case(orc, kind, W, H, K, pen, ew, iters, w_h=2, w_v=3, d_min=0):
     left, right, _ = datagen.pair(kind, W, H, K, seed=W * H + K)
