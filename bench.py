@@ -166,6 +166,24 @@ def cpu_oracle_sample(left, right, K, iters, nthreads, rows=None):
     return W * H * K * iters / dt, dt, desc
 
 
+def cpu_oracle_flow_sample(i1, i2, u_min, K, iters, nthreads, rows=None):
+    """The flow discrete stage on the CPU oracle: census of both images, the
+    decoupled costs, Dual MM on both layers; returns (cell-iter/s, s, desc)."""
+    import oracle
+    oracle.build()
+    if rows is not None:
+        i1, i2 = i1[:rows], i2[:rows]
+    H, W = i1.shape
+    t0 = time.perf_counter()
+    f1, f2 = oracle.flow_costs(oracle.census(i1), oracle.census(i2), u_min, K, u_min, K)
+    for D in (f1, f2):
+        oracle.dmm(D, W_REG, W_REG, T_REG, FBITS, iters, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    desc = (f"oracle (C, OpenMP over chains) census+decoupled flow costs+{iters} DMM iterations on both "
+            f"{W}x{H}x{K} layers ({'first %d rows of ' % rows if rows else ''}the pair), {nthreads} threads")
+    return 2 * W * H * K * iters / dt, dt, desc
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed on the host cores, same config,
     metric and unit; each step runs the whole path (census, cost volume, all
@@ -177,28 +195,34 @@ def run_reference(args):
         return
     c = datagen.CONFIGS[args.config]
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
-    if c["kind"] == "flow":
-        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for the stereo configs"}))
-        return
-    left, right, _ = datagen.pair(c["kind"], W, H, K, seed=0)
     nth = os.cpu_count() or 1
-    _, t32, _ = cpu_oracle_sample(left, right, K, iters, nth, min(32, H))
+    if c["kind"] == "flow":
+        left, right, _, _ = datagen.flow_pair(W, H, -c["d_min"], seed=0)
+        sample = lambda rows: cpu_oracle_flow_sample(left, right, c["d_min"], K, iters, nth, rows)  # noqa: E731
+        cells_per_row = 2 * W * K
+        what = f"optical flow {W}x{H}, {K}x{K} window decoupled into two {K}-label layers"
+    else:
+        left, right, _ = datagen.pair(c["kind"], W, H, K, seed=0)
+        sample = lambda rows: cpu_oracle_sample(left, right, K, iters, nth, rows)  # noqa: E731
+        cells_per_row = W * K
+        what = f"stereo {W}x{H}, {K} disparities"
+    _, t32, _ = sample(min(32, H))
     budget = 120.0
     rows = int(min(H, max(8, budget / (args.steps + args.warmup) / max(t32 / min(32, H), 1e-6))))
     for _ in range(args.warmup):
-        cpu_oracle_sample(left, right, K, iters, nth, rows)
+        sample(rows)
     times = []
     desc = ""
     for _ in range(args.steps):
-        v, dt, desc = cpu_oracle_sample(left, right, K, iters, nth, rows)
+        v, dt, desc = sample(rows)
         times.append(dt)
     ms = 1e3 * sum(times) / len(times)
-    value = W * rows * K * iters / (ms / 1e3)
+    value = cells_per_row * rows * iters / (ms / 1e3)
     line = {
         "impl": "reference", "metric": metric_for(c), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: stereo {W}x{H}, {K} disparities, census 5x5, {iters} dual iterations "
+        "config": {"workload": f"{args.config}: {what}, census 5x5, {iters} dual iterations "
                                + ("(reference arm: the whole frame per step)" if rows == H else
                                   f"(reference arm: bounded sample of the first {rows} of {H} rows per step)"),
                    "W": W, "H": H, "K": K, "iters": iters, "sample_rows": rows, "same_config": rows == H},
@@ -269,6 +293,7 @@ def main():
     lt = torch.from_numpy(Lh).to(dev)
     rt = torch.from_numpy(Rh).to(dev)
     stream = torch.cuda.current_stream(dev)
+    us = [None] * nf
 
     def step():
         if nf == 1:
@@ -278,7 +303,7 @@ def main():
         ctx.solve(iters, frame=0, nframes=nf, stream=stream)
         if args.refine:
             for f in range(nf):
-                ctx.refine(frame=f, stream=stream, energy=False)
+                us[f] = ctx.refine(frame=f, stream=stream, energy=False)[0]
 
     for _ in range(args.warmup):
         step()
@@ -364,9 +389,16 @@ def main():
         lh = torch.from_numpy(Lh).pin_memory()
         rh = torch.from_numpy(Rh).pin_memory()
         lab = torch.empty((nf, H, W), dtype=torch.uint8).pin_memory()
+        uh = torch.empty((nf, H, W), dtype=torch.float32).pin_memory()
 
         def host_step():
-            if nf == 1:
+            if args.refine:      # H2D of the images, the device step, D2H of the refined float32 u
+                lt.copy_(lh, non_blocking=True)
+                rt.copy_(rh, non_blocking=True)
+                step()
+                for f in range(nf):
+                    uh[f].copy_(us[f], non_blocking=True)
+            elif nf == 1:
                 ctx.run_host(lh[0], rh[0], iters, labels_out=lab[0], stream=stream)
             else:
                 ctx.run_host_frames(lh, rh, iters, labels_out=lab, stream=stream)
@@ -392,7 +424,8 @@ def main():
             ems = float(t.item())
         e2e = {"value": world * nf * cells * iters / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": nf * 2 * W * H,
-               "d2h_bytes_per_step": nf * (W * H + 16) if nf > 1 else W * H + 8 + 16 * iters,
+               "d2h_bytes_per_step": (nf * W * H * 4 if args.refine else
+                                      nf * (W * H + 16) if nf > 1 else W * H + 8 + 16 * iters),
                "ms_per_step": ems}
 
     cpu = None
@@ -448,9 +481,13 @@ def run_flow(args, c, world, rank, local, dev):
     stream = torch.cuda.current_stream(dev)
     t1, t2 = torch.from_numpy(i1).to(dev), torch.from_numpy(i2).to(dev)
 
+    out = {}
+
     def step():
         ctx.flow_cost_volume(t1, t2, u_min, stream=stream)
         ctx.solve(iters, frame=0, nframes=2, stream=stream)
+        if args.refine:
+            out["u"] = ctx.flow_refine(u_min, C=float(T_REG), stream=stream, energy=False)[:2]
 
     for _ in range(args.warmup):
         step()
@@ -503,18 +540,31 @@ def run_flow(args, c, world, rank, local, dev):
                                      "out_bytes_gbs": 2 * W * H * ctx.cost_volume_tensor(0).shape[2] /
                                      (flow_ms / 1e3) / 1e9},
                 "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    refine = None
+    if args.refine:
+        rms = prof["refine"][0] / prof_steps
+        # per PDHG iteration, pixel and component: the stereo iteration's 13 doubles
+        rbytes = 2 * W * H * 8 * 13 * 5 * 40
+        refine = {"ms_per_step": rms, "warps": 5, "iters": 40, "achieved_gbs": rbytes / (rms / 1e3) / 1e9,
+                  "note": "flow refinement (Eq. 19-20), both components; state L2-resident; achieved is "
+                          "algorithmic bytes / time"}
     # end to end through the public API with host buffers: H2D of both images,
-    # flow costs, both layers' Dual MM, D2H of both labellings
+    # flow costs, both layers' Dual MM (+ refinement), D2H of both labellings
+    # (or of the refined float32 flow)
     h1 = torch.from_numpy(i1).pin_memory()
     h2 = torch.from_numpy(i2).pin_memory()
-    lab = torch.empty((2, H, W), dtype=torch.uint8).pin_memory()
+    lab = torch.empty((2, H, W), dtype=torch.float32 if args.refine else torch.uint8).pin_memory()
 
     def host_step():
         t1.copy_(h1, non_blocking=True)
         t2.copy_(h2, non_blocking=True)
         step()
-        lab[0].copy_(ctx.labels(0, stream=stream), non_blocking=True)
-        lab[1].copy_(ctx.labels(1, stream=stream), non_blocking=True)
+        if args.refine:
+            lab[0].copy_(out["u"][0], non_blocking=True)
+            lab[1].copy_(out["u"][1], non_blocking=True)
+        else:
+            lab[0].copy_(ctx.labels(0, stream=stream), non_blocking=True)
+            lab[1].copy_(ctx.labels(1, stream=stream), non_blocking=True)
 
     for _ in range(2):
         host_step()
@@ -536,13 +586,14 @@ def run_flow(args, c, world, rank, local, dev):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": f"C4: optical flow {W}x{H}, {K}x{K} label window (u in [{u_min}, {u_min + K - 1}]^2), "
-                                   f"decoupled into two {K}-label layers, {iters} dual iterations each, 1 pair per GPU",
+                                   f"decoupled into two {K}-label layers, {iters} dual iterations each"
+                                   + (", continuous refinement 5 x 40" if args.refine else "") + ", 1 pair per GPU",
                        "W": W, "H": H, "K": K, "iters": iters, "fps": world / (ms / 1e3),
                        "parallelism": f"frames x{world}",
                        "l2": "flushed between timed steps (256 MB write outside events)"},
-            "roofline": roofline, "cpu_baseline": None,
+            "roofline": roofline, "refine": refine, "cpu_baseline": None,
             "e2e": {"value": world * cells * iters / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * W * H,
-                    "d2h_bytes_per_step": 2 * W * H, "ms_per_step": ems},
+                    "d2h_bytes_per_step": 2 * W * H * lab.element_size(), "ms_per_step": ems},
             "clocks": clocks, "gpu_launches": launches,
             "result": {"energy": [r[0] / (1 << FBITS) for r in res], "bound": [r[1] / (1 << FBITS) for r in res]},
         }

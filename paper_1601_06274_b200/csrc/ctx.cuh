@@ -35,6 +35,7 @@ struct RefineGraph {
     cudaGraphExec_t exec = nullptr;
     cudaStream_t cap = nullptr;
     int frame = -1;
+    int launches_per_warp = 0;
     dmm_refine_params prm{};
     float* rf = nullptr;
 };

@@ -1,6 +1,6 @@
 // refine.cu -- continuous refinement of the discrete stereo labelling (NEXT-2,
 // SURVEY 8(f)): the non-convex primal-dual method of Sec. 2.4 with
-// the two-slope data approximation of Sec. 3.1, in float32.
+// the two-slope data approximation of Sec. 3.1, in float64.
 //
 //   u+ = prox_{tau D~}(u - tau A^T (p - q))            (Eq. cont_iterates, P:306-311,
 //   q+ = prox_{tau R_-^*}(q + tau A u)                   grad A of P:350-355, d = 1)
@@ -10,14 +10,14 @@
 // Readings R24-R28 as the oracle (oracle/refine.py).
 //
 // Per pixel state (double [H][W] each): u, p_h, p_v, q_h, q_v (two buffers
-// each: every iteration reads one and writes the other, so no thread reads a
+// each: every launch reads one and writes the other, so no thread reads a
 // value another thread of the same launch updates), u0 (expansion point), s1,
-// s2 (slopes); edge arrays are indexed by the edge's first pixel.  An
-// iteration is ONE stencil kernel, one thread per pixel (the dual step's
-// neighbouring u+ are recomputed redundantly instead of a second launch); the
-// state (104 B/pixel, 48 MB at C2) stays L2-resident across iterations.  A
-// warp's `iters` iterations are captured once into a CUDA graph per (frame,
-// parameters) and replayed.
+// s2 (slopes); edge arrays are indexed by the edge's first pixel.  The
+// iterations run kHalo at a time in refine_tile_kernel (temporal blocking on
+// chip; refine_iter_kernel is the one-iteration definition it reproduces);
+// the state (104 B/pixel, 48 MB at C2) stays L2-resident across launches.  A
+// warp's launches are captured once into a CUDA graph per (frame, parameters)
+// and replayed.
 #include <cmath>
 #include <cstring>
 
@@ -151,6 +151,166 @@ __global__ void refine_iter_kernel(RefArgs a, int cur) {
     un[i] = uni;
 }
 
+// Temporal blocking: one launch runs nt <= kHalo iterations of the kernel
+// above on a kTX x kTY tile held on chip, writing back only the inner
+// (kTX - 2 kHalo) x (kTY - 2 kHalo) pixels.  Every iteration's dependence
+// cone has Chebyshev radius 1 (u+ at j reads the duals of j's left / upper
+// edges; p+, q+ of i's edges read u, u+ at i's right / lower neighbour), so
+// after nt iterations the values at distance >= nt from the tile border are
+// exactly those of nt launches of refine_iter_kernel: the same operations in
+// the same order on the same operands (bit-exact, -fmad=false).  Each thread
+// owns kTPX pixels of one column: its u, u0, s1 / s2 (or L / Q) and its
+// edges' p, q live in registers; shared memory holds what neighbours read:
+// u (two buffers: before / after the primal step) and p - q per direction
+// (the operand A^T(p - q) consumes; the subtraction is the one the iteration
+// kernel does).  Outside the image a pixel is inert; a term whose neighbour is
+// off the tile is dropped (the apron's garbage, never reaching the inner tile).
+#ifndef DMM_RT_TY
+#define DMM_RT_TY 32
+#endif
+#ifndef DMM_RT_HALO
+#define DMM_RT_HALO 4
+#endif
+#ifndef DMM_RT_TPX
+#define DMM_RT_TPX 4
+#endif
+constexpr int kTX = 64, kTY = DMM_RT_TY, kHalo = DMM_RT_HALO, kTPX = DMM_RT_TPX;
+constexpr int kTileThreads = kTX * kTY / kTPX;
+constexpr int kOX = kTX - 2 * kHalo, kOY = kTY - 2 * kHalo;
+constexpr size_t kTileSmem = 5 * sizeof(real) * kTX * kTY;
+
+// max / min / clip as numpy evaluates them on non-NaN operands (a compare and
+// a select; the libm fmax / fmin add NaN handling the finite iterates never need)
+__device__ __forceinline__ real dmax(real a, real b) { return a > b ? a : b; }
+__device__ __forceinline__ real dmin(real a, real b) { return a < b ? a : b; }
+__device__ __forceinline__ real dclip(real v, real lo, real hi) { return dmin(dmax(v, lo), hi); }
+
+// prox_conj with its loop-invariant products hoisted: aw = a * w, bs = b * step
+__device__ __forceinline__ real prox_conj_h(real t, real w, real aw, real bs) {
+    const real at = fabs(t);
+    const real tp = at <= aw ? t : copysign(dmax(aw, at - bs), t);
+    return dclip(tp, -w, w);
+}
+
+template <bool QUAD>
+__global__ void __launch_bounds__(kTileThreads) refine_tile_kernel(RefArgs a0, RefArgs a1, int cur, int nt) {
+    const RefArgs& a = blockIdx.z ? a1 : a0;
+    extern __shared__ real tsm[];            // u [2][kTY][kTX], bi, p_h - q_h, p_v - q_v
+    real* sbi = tsm + 2 * kTX * kTY;
+    real* sdh = tsm + 3 * kTX * kTY;
+    real* sdv = tsm + 4 * kTX * kTY;
+    const int W = a.W, H = a.H;
+    const real tau = a.tau, sigma = a.sigma, h = a.h, wh = a.wh, wv = a.wv;
+    const real bp = a.C + a.delta - a.eps * a.delta;
+    // the products prox_conj forms from its constant arguments, formed once
+    const real q_awh = 0.0 * wh, q_awv = 0.0 * wv, q_bs = bp * tau;
+    const real p_awh = a.eps * wh, p_awv = a.eps * wv, p_bs = a.delta * sigma;
+    const int lx = threadIdx.x % kTX, ly0 = (threadIdx.x / kTX) * kTPX;
+    const int gx = blockIdx.x * kOX - kHalo + lx, gy0 = blockIdx.y * kOY - kHalo + ly0;
+    const int b0 = 5 + 4 * cur, b1 = 5 + 4 * (1 - cur);
+    const bool inx = gx >= 0 && gx < W;
+    const bool hasr = gx + 1 < W && lx + 1 < kTX, hasl = gx > 0 && lx > 0, inr = gx + 1 < W;
+    // per pixel: u, the data term's constants c1 / c2 (stereo: tau s1, tau s2;
+    // flow: tau (Q u0 - L), 1 + tau Q -- the prox's own subexpressions), u0,
+    // the duals of the pixel's two edges
+    real u[kTPX], u0[kTPX], c1[kTPX], c2[kTPX], ph[kTPX], pv[kTPX], qh[kTPX], qv[kTPX], un[kTPX];
+#pragma unroll
+    for (int r = 0; r < kTPX; ++r) {
+        const int gy = gy0 + r, l = (ly0 + r) * kTX + lx;
+        u[r] = u0[r] = c1[r] = c2[r] = ph[r] = pv[r] = qh[r] = qv[r] = 0.0;
+        if (inx && gy >= 0 && gy < H) {
+            const size_t i = (size_t)gy * W + gx;
+            u[r] = arr(a, cur)[i];
+            u0[r] = arr(a, 2)[i];
+            const real s1 = arr(a, 3)[i], s2 = arr(a, 4)[i];
+            if constexpr (QUAD) {
+                c1[r] = tau * (s2 * u0[r] - s1);
+                c2[r] = 1.0 + tau * s2;
+            } else {
+                c1[r] = tau * s1;
+                c2[r] = tau * s2;
+            }
+            ph[r] = arr(a, b0)[i];
+            pv[r] = arr(a, b0 + 1)[i];
+            qh[r] = arr(a, b0 + 2)[i];
+            qv[r] = arr(a, b0 + 3)[i];
+        }
+        tsm[l] = u[r];
+        sdh[l] = ph[r] - qh[r];
+        sdv[l] = pv[r] - qv[r];
+    }
+    __syncthreads();
+    // all kTPX pixels are computed unconditionally (independent chains the
+    // scheduler interleaves); a pixel off the image computes on zeros and is
+    // never read by an image pixel (the neighbour tests are the image's)
+    for (int t = 0; t < nt; ++t) {
+        const real* uo = tsm + (t & 1) * (kTX * kTY);
+        real* us = tsm + ((t + 1) & 1) * (kTX * kTY);
+        real bi[kTPX];
+#pragma unroll
+        for (int r = 0; r < kTPX; ++r) {          // primal step (primal_u)
+            const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
+            real div = 0.0;
+            if (inr) div += ph[r] - qh[r];
+            if (hasl) div -= sdh[l - 1];
+            if (gy + 1 < H) div += pv[r] - qv[r];
+            if (gy > 0 && ly > 0) div -= sdv[l - kTX];
+            const real uh = u[r] - tau * div;
+            real v;
+            if constexpr (QUAD)
+                v = (uh + c1[r]) / c2[r];
+            else
+                v = uh > u0[r] + c2[r] ? uh - c2[r] : (uh < u0[r] + c1[r] ? uh - c1[r] : u0[r]);
+            un[r] = dclip(v, u0[r] - h, u0[r] + h);
+            bi[r] = 2.0 * un[r] - u[r];
+            us[l] = un[r];
+            sbi[l] = bi[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kTPX; ++r) {          // dual steps of the pixel's own edges
+            const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
+            // a neighbour's 2 u+ - u is its own bi (the same operations on the same operands)
+            if (hasr) {
+                const real ur = uo[l + 1];
+                qh[r] = prox_conj_h(qh[r] + tau * (u[r] - ur), wh, q_awh, q_bs);
+                ph[r] = prox_conj_h(ph[r] + sigma * (bi[r] - sbi[l + 1]), wh, p_awh, p_bs);
+            }
+            if (gy + 1 < H && ly + 1 < kTY) {
+                const real ud = uo[l + kTX];
+                qv[r] = prox_conj_h(qv[r] + tau * (u[r] - ud), wv, q_awv, q_bs);
+                pv[r] = prox_conj_h(pv[r] + sigma * (bi[r] - sbi[l + kTX]), wv, p_awv, p_bs);
+            }
+            u[r] = un[r];
+        }
+        // the next primal step reads the neighbours' p - q (and rewrites `uo`
+        // and bi) only after the barrier below
+#pragma unroll
+        for (int r = 0; r < kTPX; ++r) {
+            const int l = (ly0 + r) * kTX + lx;
+            sdh[l] = ph[r] - qh[r];
+            sdv[l] = pv[r] - qv[r];
+        }
+        __syncthreads();
+    }
+    if (!inx || lx < kHalo || lx >= kTX - kHalo) return;
+#pragma unroll
+    for (int r = 0; r < kTPX; ++r) {
+        const int gy = gy0 + r, ly = ly0 + r;
+        if (gy < 0 || gy >= H || ly < kHalo || ly >= kTY - kHalo) continue;
+        const size_t i = (size_t)gy * W + gx;
+        arr(a, 1 - cur)[i] = u[r];
+        if (inr) {
+            arr(a, b1)[i] = ph[r];
+            arr(a, b1 + 2)[i] = qh[r];
+        }
+        if (gy + 1 < H) {
+            arr(a, b1 + 1)[i] = pv[r];
+            arr(a, b1 + 3)[i] = qv[r];
+        }
+    }
+}
+
 __global__ void refine_swap_kernel(RefArgs a) {     // odd iteration count: the state back to buffer 0
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a.W || y >= a.H) return;
@@ -268,6 +428,29 @@ __global__ void flow_out_kernel(RefArgs a1, RefArgs a2, FlowArgs f, float* out1,
     }
 }
 
+// `iters` iterations of components a0 (and a1 when ncomp = 2) as
+// ceil(iters / kHalo) tile launches, then the state back to buffer 0; returns
+// the number of launches
+template <bool QUAD>
+int launch_iters(const RefArgs& a0, const RefArgs& a1, int ncomp, int iters, cudaStream_t s) {
+    static bool attr = [] {
+        cudaFuncSetAttribute(refine_tile_kernel<QUAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+        return true;
+    }();
+    (void)attr;
+    const dim3 grid((a0.W + kOX - 1) / kOX, (a0.H + kOY - 1) / kOY, ncomp);
+    int cur = 0, n = 0;
+    for (int it = 0; it < iters; it += kHalo, ++n, cur ^= 1)
+        refine_tile_kernel<QUAD><<<grid, kTileThreads, kTileSmem, s>>>(a0, a1, cur, min(kHalo, iters - it));
+    if (cur) {
+        const dim3 g2((a0.W + kRX - 1) / kRX, (a0.H + kRY - 1) / kRY), blk(kRX, kRY);
+        refine_swap_kernel<<<g2, blk, 0, s>>>(a0);
+        ++n;
+        if (ncomp == 2) { refine_swap_kernel<<<g2, blk, 0, s>>>(a1); ++n; }
+    }
+    return n;
+}
+
 RefArgs ref_args(dmm_ctx* ctx, int frame, const dmm_refine_params* prm) {
     FramePtrs P = frame_ptrs(ctx->L, frame);
     RefArgs a;
@@ -301,15 +484,12 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
         if (!g.cap && cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking) != cudaSuccess)
             return cuda_status(ctx, cudaGetLastError(), "refine capture stream");
         cudaGraph_t graph = nullptr;
+        int launches_per_warp = 0;
         cudaError_t e = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine capture");
         refine_warp_kernel<<<grid, blk, 0, g.cap>>>(a);
-        int cur = 0;
-        for (int it = 0; it < prm->iters; ++it) {
-            refine_iter_kernel<false><<<grid, blk, 0, g.cap>>>(a, cur);
-            cur ^= 1;
-        }
-        if (cur) refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a);
+        launches_per_warp = 1 + launch_iters<false>(a, a, 1, prm->iters, g.cap);
+        g.launches_per_warp = launches_per_warp;
         e = cudaStreamEndCapture(g.cap, &graph);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine capture end");
         e = cudaGraphInstantiate(&g.exec, graph, 0);
@@ -322,7 +502,7 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
     for (int w = 0; w < prm->warps; ++w) {
         cudaError_t e = cudaGraphLaunch(g.exec, s);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine graph launch");
-        ctx->launches += 1 + prm->iters + (prm->iters & 1);
+        ctx->launches += g.launches_per_warp;
     }
     refine_out_kernel<<<grid, blk, 0, s>>>(a, (real)ctx->cfg.d_min, out, energy_dev);
     ++ctx->launches;
@@ -350,16 +530,7 @@ dmm_status refine_flow_run(dmm_ctx* ctx, int frame, double u1_min, double u2_min
         cudaError_t e = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture");
         flow_warp_kernel<<<grid, blk, 0, g.cap>>>(a1, a2, f);
-        int cur = 0;
-        for (int it = 0; it < prm->iters; ++it) {
-            refine_iter_kernel<true><<<grid, blk, 0, g.cap>>>(a1, cur);
-            refine_iter_kernel<true><<<grid, blk, 0, g.cap>>>(a2, cur);
-            cur ^= 1;
-        }
-        if (cur) {
-            refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a1);
-            refine_swap_kernel<<<grid, blk, 0, g.cap>>>(a2);
-        }
+        g.launches_per_warp = 1 + launch_iters<true>(a1, a2, 2, prm->iters, g.cap);
         e = cudaStreamEndCapture(g.cap, &graph);
         if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture end");
         e = cudaGraphInstantiate(&g.exec, graph, 0);
@@ -372,7 +543,7 @@ dmm_status refine_flow_run(dmm_ctx* ctx, int frame, double u1_min, double u2_min
     for (int w = 0; w < prm->warps; ++w) {
         cudaError_t e = cudaGraphLaunch(g.exec, s);
         if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine graph launch");
-        ctx->launches += 1 + 2 * prm->iters + 2 * (prm->iters & 1);
+        ctx->launches += g.launches_per_warp;
     }
     flow_out_kernel<<<grid, blk, 0, s>>>(a1, a2, f, out1, out2, energy_dev);
     ++ctx->launches;

@@ -1,6 +1,7 @@
 """One warm-up + one profiled solve of a BASELINE config, for ncu captures:
 
   ncu --set full -k regex:hm2_leaf -s <skip> -c 1 python tools/one_solve.py C2
+  python tools/one_solve.py C2 2 refine      # + the continuous refinement after each solve
 """
 import os
 import sys
@@ -15,6 +16,7 @@ import paper_1601_06274_b200 as dmm  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+refine = len(sys.argv) > 3 and sys.argv[3] == "refine"
 c = datagen.CONFIGS[cfg]
 W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
 if c["kind"] == "flow":                       # configs[3]: two K-label layers of one context
@@ -25,6 +27,8 @@ if c["kind"] == "flow":                       # configs[3]: two K-label layers o
     for _ in range(reps):
         ctx.flow_cost_volume(t1, t2, c["d_min"])
         ctx.solve(iters, nframes=2)
+        if refine:
+            ctx.flow_refine(c["d_min"], C=4.0)
     torch.cuda.synchronize()
     print(cfg, ctx.result(0), ctx.result(1))
     sys.exit(0)
@@ -36,5 +40,8 @@ ctx = dmm.Context(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4
 for _ in range(reps):
     ctx.cost_volume_frames(lt, rt)
     ctx.solve(iters, nframes=nf)
+    if refine:
+        for f in range(nf):
+            ctx.refine(frame=f)
 torch.cuda.synchronize()
 print(cfg, ctx.result())
