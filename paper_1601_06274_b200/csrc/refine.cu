@@ -14,7 +14,7 @@
 // value another thread of the same launch updates), u0 (expansion point), s1,
 // s2 (slopes); edge arrays are indexed by the edge's first pixel.  The
 // iterations run kHalo at a time in refine_tile_kernel (temporal blocking on
-// chip; refine_iter_kernel is the one-iteration definition it reproduces);
+// chip);
 // the state (104 B/pixel, 48 MB at C2) stays L2-resident across launches.  A
 // warp's launches are captured once into a CUDA graph per (frame, parameters)
 // and replayed.
@@ -90,94 +90,38 @@ __global__ void refine_warp_kernel(RefArgs a) {
     arr(a, 4)[i] = s2;
 }
 
-// u+ at pixel j = (jy, jx): prox_{tau D~}(u - tau A^T (p - q)): the two-slope
-// data term of stereo (R25; slots 3/4 = s1, s2) or, QUAD, the
-// quadratic of flow (Eq. 19/20, R34; slots 3/4 = L, Q)
-template <bool QUAD>
-__device__ __forceinline__ real primal_u(const RefArgs& a, const real* u, const real* ph, const real* pv,
-                                         const real* qh, const real* qv, int jx, int jy) {
-    const int W = a.W, H = a.H;
-    const size_t j = (size_t)jy * W + jx;
-    real div = 0.0;
-    if (jx + 1 < W) div += ph[j] - qh[j];
-    if (jx > 0) div -= ph[j - 1] - qh[j - 1];
-    if (jy + 1 < H) div += pv[j] - qv[j];
-    if (jy > 0) div -= pv[j - W] - qv[j - W];
-    const real uh = u[j] - a.tau * div;
-    const real u0 = arr(a, 2)[j], s1 = arr(a, 3)[j], s2 = arr(a, 4)[j];
-    real v;
-    if constexpr (QUAD)
-        v = (uh + a.tau * (s2 * u0 - s1)) / (1.0 + a.tau * s2);
-    else
-        v = uh > u0 + a.tau * s2 ? uh - a.tau * s2 : (uh < u0 + a.tau * s1 ? uh - a.tau * s1 : u0);
-    return fmin(fmax(v, u0 - a.h), u0 + a.h);
-}
-
-// One whole iteration (Eq. cont_iterates) in one kernel: the thread of pixel
-// i computes u+ at i and at its right / down neighbours (the dual step of the
-// pixel's own edges needs them: a 3-point redundant primal instead of a second
-// launch), then q+ (from u) and p+ (from 2u+ - u) of its own edges.  Reads
-// buffer cur, writes buffer 1 - cur (u, q) and p in place (each edge owned by
-// one pixel, read by no other thread of this launch).
-template <bool QUAD>
-__global__ void refine_iter_kernel(RefArgs a, int cur) {
-    const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
-    if (x >= a.W || y >= a.H) return;
-    const int W = a.W, H = a.H;
-    const size_t i = (size_t)y * W + x;
-    const real* u = arr(a, cur);
-    real* un = arr(a, 1 - cur);
-    const int b0 = 5 + 4 * cur, b1 = 5 + 4 * (1 - cur);
-    const real* ph = arr(a, b0);
-    const real* pv = arr(a, b0 + 1);
-    const real* qh = arr(a, b0 + 2);
-    const real* qv = arr(a, b0 + 3);
-    const real ui = u[i];
-    const real uni = primal_u<QUAD>(a, u, ph, pv, qh, qv, x, y);
-    const real bp = a.C + a.delta - a.eps * a.delta;
-    const real bi = 2.0 * uni - ui;
-    if (x + 1 < W) {
-        const real unr = primal_u<QUAD>(a, u, ph, pv, qh, qv, x + 1, y);
-        const real ur = u[i + 1];
-        arr(a, b1 + 2)[i] = prox_conj(qh[i] + a.tau * (ui - ur), a.wh, 0.0, bp, a.tau);       // q+ = prox(q + tau A u)
-        arr(a, b1)[i] = prox_conj(ph[i] + a.sigma * (bi - (2.0 * unr - ur)), a.wh, a.eps, a.delta, a.sigma);
-    }
-    if (y + 1 < H) {
-        const real und = primal_u<QUAD>(a, u, ph, pv, qh, qv, x, y + 1);
-        const real ud = u[i + W];
-        arr(a, b1 + 3)[i] = prox_conj(qv[i] + a.tau * (ui - ud), a.wv, 0.0, bp, a.tau);
-        arr(a, b1 + 1)[i] = prox_conj(pv[i] + a.sigma * (bi - (2.0 * und - ud)), a.wv, a.eps, a.delta, a.sigma);
-    }
-    un[i] = uni;
-}
-
-// Temporal blocking: one launch runs nt <= kHalo iterations of the kernel
-// above on a kTX x kTY tile held on chip, writing back only the inner
-// (kTX - 2 kHalo) x (kTY - 2 kHalo) pixels.  Every iteration's dependence
-// cone has Chebyshev radius 1 (u+ at j reads the duals of j's left / upper
-// edges; p+, q+ of i's edges read u, u+ at i's right / lower neighbour), so
-// after nt iterations the values at distance >= nt from the tile border are
-// exactly those of nt launches of refine_iter_kernel: the same operations in
-// the same order on the same operands (bit-exact, -fmad=false).  Each thread
-// owns kTPX pixels of one column: its u, u0, s1 / s2 (or L / Q) and its
+// One PDHG iteration (Eq. cont_iterates), per pixel i (edges indexed by their
+// first pixel, reading buffer cur, writing 1 - cur):
+//   u+_i = clip(prox_{tau D~}(u_i - tau (A^T (p - q))_i), u0_i - h, u0_i + h)
+//          (two slopes P:431-440, R25; or the quadratic of flow, Eq. 19/20, R34)
+//   q+_e = prox_{tau R_-^*}(q_e + tau (A u)_e)
+//   p+_e = prox_{sigma R_+^*}(p_e + sigma (A (2 u+ - u))_e)
+// in the oracle's operation order (oracle/refine.py refine / flow_refine).
+//
+// Temporal blocking: one launch runs nt <= kHalo iterations on a kTX x TY
+// tile held on chip, writing back only the inner (kTX - 2 kHalo) x
+// (TY - 2 kHalo) pixels.  Every iteration's dependence cone has Chebyshev
+// radius 1 (u+ at j reads the duals of j's left / upper edges; p+, q+ of i's
+// edges read u, u+ at i's right / lower neighbour), so after nt iterations
+// the values at distance >= nt from the tile border are exactly those of nt
+// single-iteration sweeps: the same operations in the same order on the same
+// operands (bit-exact, -fmad=false).  Each thread
+// owns TPX pixels of one column: its u, u0, s1 / s2 (or L / Q) and its
 // edges' p, q live in registers; shared memory holds what neighbours read:
 // u (two buffers: before / after the primal step) and p - q per direction
 // (the operand A^T(p - q) consumes; the subtraction is the one the iteration
 // kernel does).  Outside the image a pixel is inert; a term whose neighbour is
 // off the tile is dropped (the apron's garbage, never reaching the inner tile).
-#ifndef DMM_RT_TY
-#define DMM_RT_TY 32
-#endif
-#ifndef DMM_RT_HALO
-#define DMM_RT_HALO 4
-#endif
-#ifndef DMM_RT_TPX
-#define DMM_RT_TPX 4
-#endif
-constexpr int kTX = 64, kTY = DMM_RT_TY, kHalo = DMM_RT_HALO, kTPX = DMM_RT_TPX;
-constexpr int kTileThreads = kTX * kTY / kTPX;
-constexpr int kOX = kTX - 2 * kHalo, kOY = kTY - 2 * kHalo;
-constexpr size_t kTileSmem = 5 * sizeof(real) * kTX * kTY;
+// Tile shape per data term (measured at C2 / C4): stereo 64 x 40 (5 pixels
+// per thread: 276 CTAs of 512 threads, under two waves of 148 SMs), flow
+// 64 x 32 (4 per thread: the quotient of its prox needs the registers)
+constexpr int kTX = 64, kHalo = 4;
+template <bool QUAD> struct Tile {
+    static constexpr int TY = QUAD ? 32 : 40, TPX = QUAD ? 4 : 5;
+    static constexpr int threads = kTX * TY / TPX, OY = TY - 2 * kHalo;
+    static constexpr size_t smem = 5 * sizeof(real) * kTX * TY;
+};
+constexpr int kOX = kTX - 2 * kHalo;
 
 // max / min / clip as numpy evaluates them on non-NaN operands (a compare and
 // a select; the libm fmax / fmin add NaN handling the finite iterates never need)
@@ -193,7 +137,8 @@ __device__ __forceinline__ real prox_conj_h(real t, real w, real aw, real bs) {
 }
 
 template <bool QUAD>
-__global__ void __launch_bounds__(kTileThreads) refine_tile_kernel(RefArgs a0, RefArgs a1, int cur, int nt) {
+__global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArgs a0, RefArgs a1, int cur, int nt) {
+    constexpr int kTY = Tile<QUAD>::TY, kTPX = Tile<QUAD>::TPX, kOY = Tile<QUAD>::OY;
     const RefArgs& a = blockIdx.z ? a1 : a0;
     extern __shared__ real tsm[];            // u [2][kTY][kTX], bi, p_h - q_h, p_v - q_v
     real* sbi = tsm + 2 * kTX * kTY;
@@ -248,7 +193,7 @@ __global__ void __launch_bounds__(kTileThreads) refine_tile_kernel(RefArgs a0, R
         real* us = tsm + ((t + 1) & 1) * (kTX * kTY);
         real bi[kTPX];
 #pragma unroll
-        for (int r = 0; r < kTPX; ++r) {          // primal step (primal_u)
+        for (int r = 0; r < kTPX; ++r) {          // primal step
             const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
             real div = 0.0;
             if (inr) div += ph[r] - qh[r];
@@ -434,14 +379,15 @@ __global__ void flow_out_kernel(RefArgs a1, RefArgs a2, FlowArgs f, float* out1,
 template <bool QUAD>
 int launch_iters(const RefArgs& a0, const RefArgs& a1, int ncomp, int iters, cudaStream_t s) {
     static bool attr = [] {
-        cudaFuncSetAttribute(refine_tile_kernel<QUAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+        cudaFuncSetAttribute(refine_tile_kernel<QUAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)Tile<QUAD>::smem);
         return true;
     }();
     (void)attr;
-    const dim3 grid((a0.W + kOX - 1) / kOX, (a0.H + kOY - 1) / kOY, ncomp);
+    const dim3 grid((a0.W + kOX - 1) / kOX, (a0.H + Tile<QUAD>::OY - 1) / Tile<QUAD>::OY, ncomp);
     int cur = 0, n = 0;
     for (int it = 0; it < iters; it += kHalo, ++n, cur ^= 1)
-        refine_tile_kernel<QUAD><<<grid, kTileThreads, kTileSmem, s>>>(a0, a1, cur, min(kHalo, iters - it));
+        refine_tile_kernel<QUAD><<<grid, Tile<QUAD>::threads, Tile<QUAD>::smem, s>>>(a0, a1, cur, min(kHalo, iters - it));
     if (cur) {
         const dim3 g2((a0.W + kRX - 1) / kRX, (a0.H + kRY - 1) / kRY), blk(kRX, kRY);
         refine_swap_kernel<<<g2, blk, 0, s>>>(a0);
