@@ -139,7 +139,7 @@ __device__ __forceinline__ real prox_conj_h(real t, real w, real aw, real bs) {
 template <bool QUAD>
 __global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArgs a0, RefArgs a1, int cur, int nt) {
     constexpr int kTY = Tile<QUAD>::TY, kTPX = Tile<QUAD>::TPX, kOY = Tile<QUAD>::OY;
-    const RefArgs& a = blockIdx.z ? a1 : a0;
+    const RefArgs& a = (QUAD && blockIdx.z) ? a1 : a0;     // flow: blockIdx.z = component
     extern __shared__ real tsm[];            // u [2][kTY][kTX], bi, p_h - q_h, p_v - q_v
     real* sbi = tsm + 2 * kTX * kTY;
     real* sdh = tsm + 3 * kTX * kTY;
@@ -215,17 +215,20 @@ __global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArg
 #pragma unroll
         for (int r = 0; r < kTPX; ++r) {          // dual steps of the pixel's own edges
             const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
-            // a neighbour's 2 u+ - u is its own bi (the same operations on the same operands)
-            if (hasr) {
-                const real ur = uo[l + 1];
-                qh[r] = prox_conj_h(qh[r] + tau * (u[r] - ur), wh, q_awh, q_bs);
-                ph[r] = prox_conj_h(ph[r] + sigma * (bi[r] - sbi[l + 1]), wh, p_awh, p_bs);
-            }
-            if (gy + 1 < H && ly + 1 < kTY) {
-                const real ud = uo[l + kTX];
-                qv[r] = prox_conj_h(qv[r] + tau * (u[r] - ud), wv, q_awv, q_bs);
-                pv[r] = prox_conj_h(pv[r] + sigma * (bi[r] - sbi[l + kTX]), wv, p_awv, p_bs);
-            }
+            // a neighbour's 2 u+ - u is its own bi (the same operations on the
+            // same operands).  Computed branch-free and selected: an absent
+            // edge keeps its dual (its operands, read past the row / tile end,
+            // stay inside the shared allocation and are discarded)
+            const bool hasd = gy + 1 < H && ly + 1 < kTY;
+            const real ur = uo[l + 1], ud = uo[l + kTX];
+            const real nqh = prox_conj_h(qh[r] + tau * (u[r] - ur), wh, q_awh, q_bs);
+            const real nph = prox_conj_h(ph[r] + sigma * (bi[r] - sbi[l + 1]), wh, p_awh, p_bs);
+            const real nqv = prox_conj_h(qv[r] + tau * (u[r] - ud), wv, q_awv, q_bs);
+            const real npv = prox_conj_h(pv[r] + sigma * (bi[r] - sbi[l + kTX]), wv, p_awv, p_bs);
+            qh[r] = hasr ? nqh : qh[r];
+            ph[r] = hasr ? nph : ph[r];
+            qv[r] = hasd ? nqv : qv[r];
+            pv[r] = hasd ? npv : pv[r];
             u[r] = un[r];
         }
         // the next primal step reads the neighbours' p - q (and rewrites `uo`
