@@ -193,11 +193,13 @@ DMM_API dmm_status dmm_refine(dmm_ctx* ctx, int frame, const dmm_refine_params* 
  * frame `frame + 1` (after dmm_flow_cost_volume + dmm_solve of both layers)
  * refined with the regulariser of dmm_refine on each component and the data
  * term approximated by the quadratic of Eq. 19 (central-difference gradient
- * and diagonal Hessian of the census cost at the current flow, bilinear between
- * integer displacements; readings R34-R36) with the componentwise prox of
- * Eq. 20.  float64 on the device; u1_out / u2_out (nullable) device float
- * [H][W] in pixels; energy (nullable, host) = sum D(u) + R(Au1) + R(Au2),
- * synchronises `stream` when given. */
+ * and full 2x2 Hessian of the census cost at the current flow, PSD part;
+ * bilinear between integer displacements; readings R34-R36) with the joint
+ * 2-D prox of Eq. 20 (both components iterate in lockstep).  float64 on the
+ * device; u1_out / u2_out (nullable) device float [H][W] in pixels; energy
+ * (nullable, host) = sum D(u) + R(Au1) + R(Au2), synchronises `stream` when
+ * given.  Errors: DMM_E_ARG (bad frame / parameters), DMM_E_STATE (either
+ * layer not solved, or a band-sharded context). */
 DMM_API dmm_status dmm_flow_refine(dmm_ctx* ctx, int frame, int32_t v_min, const dmm_refine_params* prm,
                                    float* u1_out, float* u2_out, double* energy, void* stream);
 

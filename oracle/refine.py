@@ -163,15 +163,19 @@ def refine(D, labels, w_h: float, w_v: float, eps: float = 1.0, delta: float = 1
 # P:134-136), the data term approximated around u0 by the quadratic of Eq. 19
 # with finite-difference gradient L and Hessian Q (step h), then
 # the prox of Eq. 20.  Readings (R34-R36):
-#   R34 the Hessian is diagonal (second differences along each component; the
-#       PSD part of a diagonal matrix is max(Q_kk, 0)), which is what makes
-#       Eq. 20's componentwise prox exact; Eq. 20's denominator "1 + tau L^k"
-#       is read as 1 + tau Q_kk (the prox of the quadratic).
+#   R34 Q is the full 2x2 finite-difference Hessian (second differences along
+#       each component, the cross difference off the diagonal), its PSD part
+#       by clipping the negative eigenvalue; the prox of Eq. 20 is the exact
+#       prox of the quadratic, (I + tau Q) u = uh + tau (Q u0 - L), then the
+#       componentwise clamp.  Eq. 20 prints the diagonal case with a garbled
+#       denominator "1 + tau L^k" (read 1 + tau Q_kk).
 #   R35 D(u) at a real displacement: bilinear interpolation of the census
 #       Hamming costs at the four surrounding integer displacements (out-of-
 #       image displacements cost oob, as in the discrete stage, R23).
 #   R36 L^k = (D(u0 + h e_k) - D(u0 - h e_k)) / (2h), Q_kk = (D(u0 + h e_k) -
-#       2 D(u0) + D(u0 - h e_k)) / h^2 (central differences), h = 1.
+#       2 D(u0) + D(u0 - h e_k)) / h^2, Q_12 = (D(u0 + h e1 + h e2) - D(u0 + h e1
+#       - h e2) - D(u0 - h e1 + h e2) + D(u0 - h e1 - h e2)) / (4 h^2) (central
+#       differences), h = 1.
 
 def _popc32(x):
     x = x.astype(np.uint32)
@@ -207,25 +211,64 @@ def flow_cost_bilinear(c1, c2, u1, u2, oob: int = 12):
     return ((1.0 - fx) * (1.0 - fy) * d00 + fx * (1.0 - fy) * d10) + ((1.0 - fx) * fy * d01 + fx * fy * d11)
 
 
-def flow_quadratic(c1, c2, u1, u2, h: float, oob: int = 12):
-    """(L1, Q11, L2, Q22) of Eq. 19 around (u1, u2) (readings R34, R36)."""
-    d0 = flow_cost_bilinear(c1, c2, u1, u2, oob)
-    dp1 = flow_cost_bilinear(c1, c2, u1 + h, u2, oob)
-    dm1 = flow_cost_bilinear(c1, c2, u1 - h, u2, oob)
-    dp2 = flow_cost_bilinear(c1, c2, u1, u2 + h, oob)
-    dm2 = flow_cost_bilinear(c1, c2, u1, u2 - h, oob)
+def psd_part(a, b, c):
+    """Positive-semidefinite part of the symmetric 2x2 [[a, b], [b, c]] (reading
+    R34): the negative eigenvalue clipped to 0.  Eigenvalues m +- rad with
+    m = (a + c)/2, rad = sqrt(((a - c)/2)^2 + b^2); when l1 = m + rad > 0 >
+    l2 = m - rad the part is l1 P1, P1 = (Q - l2 I) / (l1 - l2)."""
+    a, b, c = (np.asarray(v, np.float64) for v in (a, b, c))
+    m = 0.5 * (a + c)
+    dl = 0.5 * (a - c)
+    rad = np.sqrt(dl * dl + b * b)
+    l1 = m + rad
+    l2 = m - rad
+    mixed = (l1 > 0.0) & (l2 < 0.0)
+    s = np.where(mixed, l1 / np.where(mixed, 2.0 * rad, 1.0), 0.0)
+    pa = np.where(l2 >= 0.0, a, np.where(mixed, s * (a - l2), 0.0))
+    pb = np.where(l2 >= 0.0, b, np.where(mixed, s * b, 0.0))
+    pc = np.where(l2 >= 0.0, c, np.where(mixed, s * (c - l2), 0.0))
+    return pa, pb, pc
+
+
+def flow_quadratic(c1, c2, u1, u2, h: float, oob: int = 12, cost=None):
+    """(L1, L2, Qa, Qb, Qc) of Eq. 19 around (u1, u2) (readings R34, R36): the
+    central-difference gradient and Hessian [[Qa, Qb], [Qb, Qc]] of D (step h),
+    PSD part.  `cost(u1, u2)` defaults to the bilinear census cost (R35)."""
+    if cost is None:
+        cost = lambda v1, v2: flow_cost_bilinear(c1, c2, v1, v2, oob)  # noqa: E731
+    d0 = cost(u1, u2)
+    dp1 = cost(u1 + h, u2)
+    dm1 = cost(u1 - h, u2)
+    dp2 = cost(u1, u2 + h)
+    dm2 = cost(u1, u2 - h)
+    dpp = cost(u1 + h, u2 + h)
+    dpm = cost(u1 + h, u2 - h)
+    dmp = cost(u1 - h, u2 + h)
+    dmm = cost(u1 - h, u2 - h)
     L1 = (dp1 - dm1) / (2.0 * h)
     L2 = (dp2 - dm2) / (2.0 * h)
-    Q1 = np.maximum((dp1 - 2.0 * d0 + dm1) / (h * h), 0.0)
-    Q2 = np.maximum((dp2 - 2.0 * d0 + dm2) / (h * h), 0.0)
-    return L1, Q1, L2, Q2
+    a = (dp1 - 2.0 * d0 + dm1) / (h * h)
+    c = (dp2 - 2.0 * d0 + dm2) / (h * h)
+    b = ((dpp - dpm) - (dmp - dmm)) / (4.0 * h * h)
+    Qa, Qb, Qc = psd_part(a, b, c)
+    return L1, L2, Qa, Qb, Qc
 
 
-def prox_quadratic(uh, u0, L, Q, tau: float, h: float):
-    """Prox of tau * D~ for the quadratic of Eq. 19 per component (Eq. 20 with
-    reading R34), then the clamp to [u0 - h, u0 + h]."""
-    v = (uh + tau * (Q * u0 - L)) / (1.0 + tau * Q)
-    return np.clip(v, u0 - h, u0 + h)
+def prox_quadratic(uh1, uh2, u01, u02, L1, L2, Qa, Qb, Qc, tau: float, h: float):
+    """Prox of tau * D~ for the quadratic of Eq. 19 (Eq. 20, reading R34): the
+    minimiser of tau (L^T (u - u0) + (u - u0)^T Q (u - u0) / 2) + |u - uh|^2 / 2,
+    i.e. (I + tau Q) u = uh + tau (Q u0 - L) solved by Cramer's rule, then each
+    component clamped to [u0 - h, u0 + h] (Eq. 20's clamp).  For a diagonal Q
+    this is Eq. 20's componentwise quotient with the denominator 1 + tau Q_kk."""
+    r1 = uh1 + tau * ((Qa * u01 + Qb * u02) - L1)
+    r2 = uh2 + tau * ((Qb * u01 + Qc * u02) - L2)
+    a11 = 1.0 + tau * Qa
+    a22 = 1.0 + tau * Qc
+    a12 = tau * Qb
+    det = a11 * a22 - a12 * a12
+    v1 = (a22 * r1 - a12 * r2) / det
+    v2 = (a11 * r2 - a12 * r1) / det
+    return np.clip(v1, u01 - h, u01 + h), np.clip(v2, u02 - h, u02 + h)
 
 
 def flow_energy(c1, c2, u1, u2, w_h, w_v, eps, delta, C, oob: int = 12):
@@ -240,9 +283,11 @@ def flow_refine(c1, c2, u1, u2, w_h: float, w_v: float, eps: float = 1.0, delta:
                 h: float = 1.0, tau: float = 0.35, sigma: float = 0.35, warps: int = 5, iters: int = 40,
                 oob: int = 12):
     """Refine an integer flow field (u1, u2) (pixels).  Per warp the quadratic
-    model is rebuilt at the current u; each component then runs the same
-    iterates as the stereo refinement with the quadratic prox (the components
-    couple only through the re-linearisation).  Returns (u1, u2, energy)."""
+    model is rebuilt at the current u; then `iters` iterations of the stereo
+    refinement's PDHG run on both components in lockstep: the primal step's
+    prox is the joint 2-D prox of Eq. 20 (the components couple there and in
+    the model), the duals p, q of each component's regulariser are separate
+    (Eq. regularizer-form sums r over k = 1, 2).  Returns (u1, u2, energy)."""
     c1 = np.asarray(c1, np.uint32)
     c2 = np.asarray(c2, np.uint32)
     H, W = c1.shape
@@ -251,20 +296,18 @@ def flow_refine(c1, c2, u1, u2, w_h: float, w_v: float, eps: float = 1.0, delta:
           for _ in range(2)]
     bp = C + delta - eps * delta
     for _ in range(warps):
-        L1, Q1, L2, Q2 = flow_quadratic(c1, c2, us[0], us[1], h, oob)
-        for k, (L, Q) in enumerate(((L1, Q1), (L2, Q2))):
-            u = us[k]
-            u0 = u.copy()
-            s = st[k]
-            for _ in range(iters):
-                uh = u - tau * AT(s["ph"] - s["qh"], s["pv"] - s["qv"], (H, W))
-                u_new = prox_quadratic(uh, u0, L, Q, tau, h)
+        L1, L2, Qa, Qb, Qc = flow_quadratic(c1, c2, us[0], us[1], h, oob)
+        u01, u02 = us[0].copy(), us[1].copy()
+        for _ in range(iters):
+            uh = [us[k] - tau * AT(st[k]["ph"] - st[k]["qh"], st[k]["pv"] - st[k]["qv"], (H, W)) for k in range(2)]
+            un = prox_quadratic(uh[0], uh[1], u01, u02, L1, L2, Qa, Qb, Qc, tau, h)
+            for k in range(2):
+                s, u = st[k], us[k]
                 ah, av = A(u)
                 s["qh"] = prox_conj(s["qh"] + tau * ah, w_h, 0.0, bp, tau)
                 s["qv"] = prox_conj(s["qv"] + tau * av, w_v, 0.0, bp, tau)
-                bh, bv = A(2.0 * u_new - u)
+                bh, bv = A(2.0 * un[k] - u)
                 s["ph"] = prox_conj(s["ph"] + sigma * bh, w_h, eps, delta, sigma)
                 s["pv"] = prox_conj(s["pv"] + sigma * bv, w_v, eps, delta, sigma)
-                u = u_new
-            us[k] = u
+            us = [un[0], un[1]]
     return us[0], us[1], flow_energy(c1, c2, us[0], us[1], w_h, w_v, eps, delta, C, oob)

@@ -15,7 +15,7 @@
 // s2 (slopes); edge arrays are indexed by the edge's first pixel.  The
 // iterations run kHalo at a time in refine_tile_kernel (temporal blocking on
 // chip);
-// the state (104 B/pixel, 48 MB at C2) stays L2-resident across launches.  A
+// the state (112 B/pixel, 52 MB at C2) stays L2-resident across launches.  A
 // warp's launches are captured once into a CUDA graph per (frame, parameters)
 // and replayed.
 #include <cmath>
@@ -28,8 +28,9 @@ namespace dmm {
 namespace {
 
 constexpr int kRX = 32, kRY = 8;
-// u (buffers 0, 1), u0 (expansion point), s1, s2, then per buffer b: ph, pv, qh, qv at 5 + 4b
-constexpr int kRefArrays = 13;
+// u (buffers 0, 1), u0 (expansion point), s1, s2 (flow: L, Q_kk), then per
+// buffer b: ph, pv, qh, qv at 5 + 4b; 13: flow's Q_12 (first component's area)
+constexpr int kRefArrays = 14;
 using real = double;             // float64, the oracle's precision
 
 struct RefArgs {
@@ -112,16 +113,11 @@ __global__ void refine_warp_kernel(RefArgs a) {
 // (the operand A^T(p - q) consumes; the subtraction is the one the iteration
 // kernel does).  Outside the image a pixel is inert; a term whose neighbour is
 // off the tile is dropped (the apron's garbage, never reaching the inner tile).
-// Tile shape per data term (measured at C2 / C4): stereo 64 x 40 (5 pixels
-// per thread: 276 CTAs of 512 threads, under two waves of 148 SMs), flow
-// 64 x 32 (4 per thread: the quotient of its prox needs the registers)
-constexpr int kTX = 64, kHalo = 4;
-template <bool QUAD> struct Tile {
-    static constexpr int TY = QUAD ? 32 : 40, TPX = QUAD ? 4 : 5;
-    static constexpr int threads = kTX * TY / TPX, OY = TY - 2 * kHalo;
-    static constexpr size_t smem = 5 * sizeof(real) * kTX * TY;
-};
-constexpr int kOX = kTX - 2 * kHalo;
+// Stereo tile 64 x 40, 5 pixels per thread: 276 CTAs of 512 threads at C2,
+// under two waves of 148 SMs (measured against 64 x 32 / 4 and 64 x 48 / 6)
+constexpr int kTX = 64, kHalo = 4, kTY = 40, kTPX = 5;
+constexpr int kTileThreads = kTX * kTY / kTPX, kOX = kTX - 2 * kHalo, kOY = kTY - 2 * kHalo;
+constexpr size_t kTileSmem = 5 * sizeof(real) * kTX * kTY;
 
 // max / min / clip as numpy evaluates them on non-NaN operands (a compare and
 // a select; the libm fmax / fmin add NaN handling the finite iterates never need)
@@ -136,10 +132,7 @@ __device__ __forceinline__ real prox_conj_h(real t, real w, real aw, real bs) {
     return dclip(tp, -w, w);
 }
 
-template <bool QUAD>
-__global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArgs a0, RefArgs a1, int cur, int nt) {
-    constexpr int kTY = Tile<QUAD>::TY, kTPX = Tile<QUAD>::TPX, kOY = Tile<QUAD>::OY;
-    const RefArgs& a = (QUAD && blockIdx.z) ? a1 : a0;     // flow: blockIdx.z = component
+__global__ void __launch_bounds__(kTileThreads) refine_tile_kernel(RefArgs a, int cur, int nt) {
     extern __shared__ real tsm[];            // u [2][kTY][kTX], bi, p_h - q_h, p_v - q_v
     real* sbi = tsm + 2 * kTX * kTY;
     real* sdh = tsm + 3 * kTX * kTY;
@@ -155,9 +148,8 @@ __global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArg
     const int b0 = 5 + 4 * cur, b1 = 5 + 4 * (1 - cur);
     const bool inx = gx >= 0 && gx < W;
     const bool hasr = gx + 1 < W && lx + 1 < kTX, hasl = gx > 0 && lx > 0, inr = gx + 1 < W;
-    // per pixel: u, the data term's constants c1 / c2 (stereo: tau s1, tau s2;
-    // flow: tau (Q u0 - L), 1 + tau Q -- the prox's own subexpressions), u0,
-    // the duals of the pixel's two edges
+    // per pixel: u, the data prox's constants c1 = tau s1, c2 = tau s2 (its
+    // own subexpressions), u0, the duals of the pixel's two edges
     real u[kTPX], u0[kTPX], c1[kTPX], c2[kTPX], ph[kTPX], pv[kTPX], qh[kTPX], qv[kTPX], un[kTPX];
 #pragma unroll
     for (int r = 0; r < kTPX; ++r) {
@@ -167,14 +159,8 @@ __global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArg
             const size_t i = (size_t)gy * W + gx;
             u[r] = arr(a, cur)[i];
             u0[r] = arr(a, 2)[i];
-            const real s1 = arr(a, 3)[i], s2 = arr(a, 4)[i];
-            if constexpr (QUAD) {
-                c1[r] = tau * (s2 * u0[r] - s1);
-                c2[r] = 1.0 + tau * s2;
-            } else {
-                c1[r] = tau * s1;
-                c2[r] = tau * s2;
-            }
+            c1[r] = tau * arr(a, 3)[i];
+            c2[r] = tau * arr(a, 4)[i];
             ph[r] = arr(a, b0)[i];
             pv[r] = arr(a, b0 + 1)[i];
             qh[r] = arr(a, b0 + 2)[i];
@@ -201,11 +187,7 @@ __global__ void __launch_bounds__(Tile<QUAD>::threads) refine_tile_kernel(RefArg
             if (gy + 1 < H) div += pv[r] - qv[r];
             if (gy > 0 && ly > 0) div -= sdv[l - kTX];
             const real uh = u[r] - tau * div;
-            real v;
-            if constexpr (QUAD)
-                v = (uh + c1[r]) / c2[r];
-            else
-                v = uh > u0[r] + c2[r] ? uh - c2[r] : (uh < u0[r] + c1[r] ? uh - c1[r] : u0[r]);
+            const real v = uh > u0[r] + c2[r] ? uh - c2[r] : (uh < u0[r] + c1[r] ? uh - c1[r] : u0[r]);
             un[r] = dclip(v, u0[r] - h, u0[r] + h);
             bi[r] = 2.0 * un[r] - u[r];
             us[l] = un[r];
@@ -329,8 +311,11 @@ __global__ void flow_init_kernel(RefArgs a1, RefArgs a2, real u1_min, real u2_mi
     for (int k = 5; k < kRefArrays; ++k) { arr(a1, k)[i] = 0.0; arr(a2, k)[i] = 0.0; }
 }
 
-// the quadratic model of Eq. 19 at the current (u1, u2) (readings R34, R36):
-// u0 -> slot 2, L -> slot 3, Q (PSD part) -> slot 4 of each component
+// the quadratic model of Eq. 19 at the current (u1, u2) (readings R34-R36):
+// central differences (nine bilinear census costs), the PSD part of the 2x2
+// Hessian [[Qa, Qb], [Qb, Qc]] (negative eigenvalue clipped), in the oracle's
+// operation order (oracle/refine.py flow_quadratic, psd_part).  Slots: u0 ->
+// 2, L -> 3 of each component, Qa -> a1's 4, Qc -> a2's 4, Qb -> a1's 13.
 __global__ void flow_warp_kernel(RefArgs a1, RefArgs a2, FlowArgs f) {
     const int x = blockIdx.x * kRX + threadIdx.x, y = blockIdx.y * kRY + threadIdx.y;
     if (x >= a1.W || y >= a1.H) return;
@@ -339,12 +324,174 @@ __global__ void flow_warp_kernel(RefArgs a1, RefArgs a2, FlowArgs f) {
     const real d0 = flow_cost_bilinear(f, x, y, u1, u2);
     const real dp1 = flow_cost_bilinear(f, x, y, u1 + h, u2), dm1 = flow_cost_bilinear(f, x, y, u1 - h, u2);
     const real dp2 = flow_cost_bilinear(f, x, y, u1, u2 + h), dm2 = flow_cost_bilinear(f, x, y, u1, u2 - h);
+    const real dpp = flow_cost_bilinear(f, x, y, u1 + h, u2 + h), dpm = flow_cost_bilinear(f, x, y, u1 + h, u2 - h);
+    const real dmp = flow_cost_bilinear(f, x, y, u1 - h, u2 + h), dmm = flow_cost_bilinear(f, x, y, u1 - h, u2 - h);
+    const real qa = (dp1 - 2.0 * d0 + dm1) / (h * h);
+    const real qc = (dp2 - 2.0 * d0 + dm2) / (h * h);
+    const real qb = ((dpp - dpm) - (dmp - dmm)) / (4.0 * h * h);
+    // PSD part: eigenvalues m +- rad; l1 > 0 > l2 keeps l1 (Q - l2 I) / (l1 - l2)
+    const real m = 0.5 * (qa + qc), dl = 0.5 * (qa - qc);
+    const real rad = sqrt(dl * dl + qb * qb);
+    const real l1 = m + rad, l2 = m - rad;
+    const bool mixed = l1 > 0.0 && l2 < 0.0;
+    const real sc = mixed ? l1 / (2.0 * rad) : 0.0;
     arr(a1, 2)[i] = u1;
     arr(a1, 3)[i] = (dp1 - dm1) / (2.0 * h);
-    arr(a1, 4)[i] = fmax((dp1 - 2.0 * d0 + dm1) / (h * h), 0.0);
+    arr(a1, 4)[i] = l2 >= 0.0 ? qa : (mixed ? sc * (qa - l2) : 0.0);
+    arr(a1, 13)[i] = l2 >= 0.0 ? qb : (mixed ? sc * qb : 0.0);
     arr(a2, 2)[i] = u2;
     arr(a2, 3)[i] = (dp2 - dm2) / (2.0 * h);
-    arr(a2, 4)[i] = fmax((dp2 - 2.0 * d0 + dm2) / (h * h), 0.0);
+    arr(a2, 4)[i] = l2 >= 0.0 ? qc : (mixed ? sc * (qc - l2) : 0.0);
+}
+
+// Flow tile kernel: the stereo tile kernel's temporal blocking with both
+// components in lockstep, because the primal step is the joint 2-D prox of
+// Eq. 20 (reading R34): r = uh + tau (Q u0 - L), (I + tau Q) v = r by Cramer's
+// rule, each component clamped to [u0 - h, u0 + h]; each component's duals
+// (its own regulariser) as in stereo.  Per-pixel constants of the prox (u0,
+// tau (Q u0 - L), the entries and determinant of I + tau Q) live in shared
+// memory, the duals in registers, u (before / after the primal step) and
+// p - q per component and direction in shared memory.  Tile 64 x 24, three
+// pixels per thread.
+constexpr int kFTY = 24, kFTPX = 3, kFOY = kFTY - 2 * kHalo;
+constexpr int kFThreads = kTX * kFTY / kFTPX, kFN = kTX * kFTY;
+constexpr size_t kFSmem = 16 * sizeof(real) * kFN;
+
+__global__ void __launch_bounds__(kFThreads) flow_tile_kernel(RefArgs a1, RefArgs a2, int cur, int nt) {
+    extern __shared__ real fsm[];
+    // [0, 4): u1 (2 buffers), u2 (2 buffers); [4, 8): dh1, dv1, dh2, dv2;
+    // [8, 16): u01, u02, k1, k2, m11, m22, m12, det
+    auto S = [&](int k) { return fsm + (size_t)k * kFN; };
+    const int W = a1.W, H = a1.H;
+    const real tau = a1.tau, sigma = a1.sigma, h = a1.h, wh = a1.wh, wv = a1.wv;
+    const real bp = a1.C + a1.delta - a1.eps * a1.delta;
+    const real q_awh = 0.0 * wh, q_awv = 0.0 * wv, q_bs = bp * tau;
+    const real p_awh = a1.eps * wh, p_awv = a1.eps * wv, p_bs = a1.delta * sigma;
+    const int lx = threadIdx.x % kTX, ly0 = (threadIdx.x / kTX) * kFTPX;
+    const int gx = blockIdx.x * kOX - kHalo + lx, gy0 = blockIdx.y * kFOY - kHalo + ly0;
+    const int b0 = 5 + 4 * cur, b1 = 5 + 4 * (1 - cur);
+    const bool inx = gx >= 0 && gx < W;
+    const bool hasr = gx + 1 < W && lx + 1 < kTX, hasl = gx > 0 && lx > 0, inr = gx + 1 < W;
+    real u[2][kFTPX], ph[2][kFTPX], pv[2][kFTPX], qh[2][kFTPX], qv[2][kFTPX], un[2][kFTPX];
+#pragma unroll
+    for (int r = 0; r < kFTPX; ++r) {
+        const int gy = gy0 + r, l = (ly0 + r) * kTX + lx;
+        real u01 = 0.0, u02 = 0.0, k1 = 0.0, k2 = 0.0, m11 = 1.0, m22 = 1.0, m12 = 0.0, det = 1.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) u[c][r] = ph[c][r] = pv[c][r] = qh[c][r] = qv[c][r] = 0.0;
+        if (inx && gy >= 0 && gy < H) {
+            const size_t i = (size_t)gy * W + gx;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const RefArgs& a = c ? a2 : a1;
+                u[c][r] = arr(a, cur)[i];
+                ph[c][r] = arr(a, b0)[i];
+                pv[c][r] = arr(a, b0 + 1)[i];
+                qh[c][r] = arr(a, b0 + 2)[i];
+                qv[c][r] = arr(a, b0 + 3)[i];
+            }
+            u01 = arr(a1, 2)[i];
+            u02 = arr(a2, 2)[i];
+            const real L1 = arr(a1, 3)[i], L2 = arr(a2, 3)[i];
+            const real qa = arr(a1, 4)[i], qc = arr(a2, 4)[i], qb = arr(a1, 13)[i];
+            // the prox's subexpressions, as oracle/refine.py prox_quadratic forms them
+            k1 = tau * ((qa * u01 + qb * u02) - L1);
+            k2 = tau * ((qb * u01 + qc * u02) - L2);
+            m11 = 1.0 + tau * qa;
+            m22 = 1.0 + tau * qc;
+            m12 = tau * qb;
+            det = m11 * m22 - m12 * m12;
+        }
+        S(8)[l] = u01; S(9)[l] = u02; S(10)[l] = k1; S(11)[l] = k2;
+        S(12)[l] = m11; S(13)[l] = m22; S(14)[l] = m12; S(15)[l] = det;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            S(2 * c)[l] = u[c][r];
+            S(4 + 2 * c)[l] = ph[c][r] - qh[c][r];
+            S(5 + 2 * c)[l] = pv[c][r] - qv[c][r];
+        }
+    }
+    __syncthreads();
+    for (int t = 0; t < nt; ++t) {
+        const int ob = t & 1, nb = (t + 1) & 1;      // u buffers: old, new
+#pragma unroll
+        for (int r = 0; r < kFTPX; ++r) {          // joint primal step
+            const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
+            real uh[2];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const real* sdh = S(4 + 2 * c);
+                const real* sdv = S(5 + 2 * c);
+                real div = 0.0;
+                if (inr) div += ph[c][r] - qh[c][r];
+                if (hasl) div -= sdh[l - 1];
+                if (gy + 1 < H) div += pv[c][r] - qv[c][r];
+                if (gy > 0 && ly > 0) div -= sdv[l - kTX];
+                uh[c] = u[c][r] - tau * div;
+            }
+            const real u01 = S(8)[l], u02 = S(9)[l];
+            const real m11 = S(12)[l], m22 = S(13)[l], m12 = S(14)[l], det = S(15)[l];
+            const real r1 = uh[0] + S(10)[l], r2 = uh[1] + S(11)[l];
+            const real v1 = (m22 * r1 - m12 * r2) / det;
+            const real v2 = (m11 * r2 - m12 * r1) / det;
+            un[0][r] = dclip(v1, u01 - h, u01 + h);
+            un[1][r] = dclip(v2, u02 - h, u02 + h);
+            S(2 * 0 + nb)[l] = un[0][r];
+            S(2 * 1 + nb)[l] = un[1][r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kFTPX; ++r) {          // each component's dual steps
+            const int gy = gy0 + r, ly = ly0 + r, l = ly * kTX + lx;
+            const bool hasd = gy + 1 < H && ly + 1 < kFTY;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const real* uo = S(2 * c + ob);
+                const real* us = S(2 * c + nb);
+                const real bi = 2.0 * un[c][r] - u[c][r];
+                const real ur = uo[l + 1], ud = uo[l + kTX];
+                const real nqh = prox_conj_h(qh[c][r] + tau * (u[c][r] - ur), wh, q_awh, q_bs);
+                const real nph = prox_conj_h(ph[c][r] + sigma * (bi - (2.0 * us[l + 1] - ur)), wh, p_awh, p_bs);
+                const real nqv = prox_conj_h(qv[c][r] + tau * (u[c][r] - ud), wv, q_awv, q_bs);
+                const real npv = prox_conj_h(pv[c][r] + sigma * (bi - (2.0 * us[l + kTX] - ud)), wv, p_awv, p_bs);
+                qh[c][r] = hasr ? nqh : qh[c][r];
+                ph[c][r] = hasr ? nph : ph[c][r];
+                qv[c][r] = hasd ? nqv : qv[c][r];
+                pv[c][r] = hasd ? npv : pv[c][r];
+                u[c][r] = un[c][r];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kFTPX; ++r) {
+            const int l = (ly0 + r) * kTX + lx;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                S(4 + 2 * c)[l] = ph[c][r] - qh[c][r];
+                S(5 + 2 * c)[l] = pv[c][r] - qv[c][r];
+            }
+        }
+        __syncthreads();
+    }
+    if (!inx || lx < kHalo || lx >= kTX - kHalo) return;
+#pragma unroll
+    for (int r = 0; r < kFTPX; ++r) {
+        const int gy = gy0 + r, ly = ly0 + r;
+        if (gy < 0 || gy >= H || ly < kHalo || ly >= kFTY - kHalo) continue;
+        const size_t i = (size_t)gy * W + gx;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const RefArgs& a = c ? a2 : a1;
+            arr(a, 1 - cur)[i] = u[c][r];
+            if (inr) {
+                arr(a, b1)[i] = ph[c][r];
+                arr(a, b1 + 2)[i] = qh[c][r];
+            }
+            if (gy + 1 < H) {
+                arr(a, b1 + 1)[i] = pv[c][r];
+                arr(a, b1 + 3)[i] = qv[c][r];
+            }
+        }
+    }
 }
 
 __global__ void flow_out_kernel(RefArgs a1, RefArgs a2, FlowArgs f, float* out1, float* out2, double* energy) {
@@ -376,26 +523,31 @@ __global__ void flow_out_kernel(RefArgs a1, RefArgs a2, FlowArgs f, float* out1,
     }
 }
 
-// `iters` iterations of components a0 (and a1 when ncomp = 2) as
-// ceil(iters / kHalo) tile launches, then the state back to buffer 0; returns
-// the number of launches
-template <bool QUAD>
-int launch_iters(const RefArgs& a0, const RefArgs& a1, int ncomp, int iters, cudaStream_t s) {
+// `iters` iterations as ceil(iters / kHalo) tile launches (stereo: a0; flow:
+// a0, a1 = the two components), then the state back to buffer 0; returns the
+// number of launches
+int launch_iters(const RefArgs& a0, const RefArgs* a1, int iters, cudaStream_t s) {
     static bool attr = [] {
-        cudaFuncSetAttribute(refine_tile_kernel<QUAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)Tile<QUAD>::smem);
+        cudaFuncSetAttribute(refine_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+        cudaFuncSetAttribute(flow_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFSmem);
         return true;
     }();
     (void)attr;
-    const dim3 grid((a0.W + kOX - 1) / kOX, (a0.H + Tile<QUAD>::OY - 1) / Tile<QUAD>::OY, ncomp);
     int cur = 0, n = 0;
-    for (int it = 0; it < iters; it += kHalo, ++n, cur ^= 1)
-        refine_tile_kernel<QUAD><<<grid, Tile<QUAD>::threads, Tile<QUAD>::smem, s>>>(a0, a1, cur, min(kHalo, iters - it));
+    for (int it = 0; it < iters; it += kHalo, ++n, cur ^= 1) {
+        const int nt = min(kHalo, iters - it);
+        if (a1)
+            flow_tile_kernel<<<dim3((a0.W + kOX - 1) / kOX, (a0.H + kFOY - 1) / kFOY), kFThreads, kFSmem, s>>>(
+                a0, *a1, cur, nt);
+        else
+            refine_tile_kernel<<<dim3((a0.W + kOX - 1) / kOX, (a0.H + kOY - 1) / kOY), kTileThreads, kTileSmem, s>>>(
+                a0, cur, nt);
+    }
     if (cur) {
         const dim3 g2((a0.W + kRX - 1) / kRX, (a0.H + kRY - 1) / kRY), blk(kRX, kRY);
         refine_swap_kernel<<<g2, blk, 0, s>>>(a0);
         ++n;
-        if (ncomp == 2) { refine_swap_kernel<<<g2, blk, 0, s>>>(a1); ++n; }
+        if (a1) { refine_swap_kernel<<<g2, blk, 0, s>>>(*a1); ++n; }
     }
     return n;
 }
@@ -437,7 +589,7 @@ dmm_status refine_run(dmm_ctx* ctx, int frame, const dmm_refine_params* prm, flo
         cudaError_t e = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine capture");
         refine_warp_kernel<<<grid, blk, 0, g.cap>>>(a);
-        launches_per_warp = 1 + launch_iters<false>(a, a, 1, prm->iters, g.cap);
+        launches_per_warp = 1 + launch_iters(a, nullptr, prm->iters, g.cap);
         g.launches_per_warp = launches_per_warp;
         e = cudaStreamEndCapture(g.cap, &graph);
         if (e != cudaSuccess) return cuda_status(ctx, e, "refine capture end");
@@ -479,7 +631,7 @@ dmm_status refine_flow_run(dmm_ctx* ctx, int frame, double u1_min, double u2_min
         cudaError_t e = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
         if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture");
         flow_warp_kernel<<<grid, blk, 0, g.cap>>>(a1, a2, f);
-        g.launches_per_warp = 1 + launch_iters<true>(a1, a2, 2, prm->iters, g.cap);
+        g.launches_per_warp = 1 + launch_iters(a1, &a2, prm->iters, g.cap);
         e = cudaStreamEndCapture(g.cap, &graph);
         if (e != cudaSuccess) return cuda_status(ctx, e, "flow refine capture end");
         e = cudaGraphInstantiate(&g.exec, graph, 0);

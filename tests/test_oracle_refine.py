@@ -129,31 +129,99 @@ def test_flow_cost_bilinear_at_integers_is_the_census_cost(orc):
         assert np.array_equal(best, f1[:, :, a + 8].astype(np.float64))
 
 
+def test_psd_part_is_eigenvalue_clipping():
+    """psd_part's closed form equals V max(Lambda, 0) V^T by numpy's eigh."""
+    rng = np.random.default_rng(6)
+    for _ in range(500):
+        a, b, c = rng.normal(scale=10, size=3)
+        if rng.random() < 0.2:
+            b = 0.0
+        lam, V = np.linalg.eigh(np.array([[a, b], [b, c]]))
+        ref = V @ np.diag(np.maximum(lam, 0.0)) @ V.T
+        pa, pb, pc = rf.psd_part(a, b, c)
+        assert np.allclose([[pa, pb], [pb, pc]], ref, atol=1e-9 * (1 + np.abs(lam).max()))
+    # already PSD: unchanged (bit-exact); negative definite: 0
+    assert tuple(map(float, rf.psd_part(4.0, 1.0, 3.0))) == (4.0, 1.0, 3.0)
+    assert tuple(map(float, rf.psd_part(-4.0, 1.0, -3.0))) == (0.0, 0.0, 0.0)
+
+
+def test_flow_quadratic_recovers_a_quadratic_cost():
+    """Central differences are exact on a quadratic: D(u) = g^T u + u^T B u / 2
+    gives L = g + B u and Q = PSD part of B (a saddle B is clipped)."""
+    rng = np.random.default_rng(7)
+    u1 = rng.uniform(-5, 5, size=(4, 5))
+    u2 = rng.uniform(-5, 5, size=(4, 5))
+    for B in (np.array([[3.0, 1.0], [1.0, 2.0]]), np.array([[2.0, 3.0], [3.0, -1.0]]),
+              np.array([[-1.0, 0.5], [0.5, -2.0]])):
+        g = np.array([0.7, -1.3])
+        cost = lambda v1, v2: g[0] * v1 + g[1] * v2 + 0.5 * (B[0, 0] * v1 * v1 + 2 * B[0, 1] * v1 * v2 + B[1, 1] * v2 * v2)  # noqa: E731
+        L1, L2, Qa, Qb, Qc = rf.flow_quadratic(None, None, u1, u2, 1.0, cost=cost)
+        assert np.allclose(L1, g[0] + B[0, 0] * u1 + B[0, 1] * u2, atol=1e-9)
+        assert np.allclose(L2, g[1] + B[1, 0] * u1 + B[1, 1] * u2, atol=1e-9)
+        lam, V = np.linalg.eigh(B)
+        P = V @ np.diag(np.maximum(lam, 0.0)) @ V.T
+        assert np.allclose(Qa, P[0, 0], atol=1e-9) and np.allclose(Qb, P[0, 1], atol=1e-9)
+        assert np.allclose(Qc, P[1, 1], atol=1e-9)
+
+
 def test_prox_quadratic_by_grid_search():
+    """Eq. 20's prox: (a) a diagonal Q separates, so the clamped quotient is the
+    exact box-constrained prox (1-D grid search per component); (b) a general
+    PSD Q with the box inactive is the unconstrained prox (2-D grid search)."""
     rng = np.random.default_rng(5)
-    for _ in range(300):
-        u0, L, Q = rng.uniform(-10, 10), rng.uniform(-20, 20), rng.uniform(0, 30)
+    for _ in range(200):
+        u0 = rng.uniform(-10, 10, 2)
+        L = rng.uniform(-20, 20, 2)
+        Qd = rng.uniform(0, 30, 2)
         tau, h = rng.uniform(0.05, 1.0), rng.uniform(0.5, 2.0)
-        uh = u0 + rng.uniform(-5, 5)
-        grid = np.linspace(u0 - h, u0 + h, 20001)
-        obj = tau * (L * (grid - u0) + 0.5 * Q * (grid - u0) ** 2) + 0.5 * (grid - uh) ** 2
-        got = rf.prox_quadratic(np.array([uh]), np.array([u0]), np.array([L]), np.array([Q]), tau, h)[0]
-        assert abs(got - grid[np.argmin(obj)]) < 2e-4
+        uh = u0 + rng.uniform(-5, 5, 2)
+        got = rf.prox_quadratic(uh[0], uh[1], u0[0], u0[1], L[0], L[1], Qd[0], 0.0, Qd[1], tau, h)
+        for k in range(2):
+            grid = np.linspace(u0[k] - h, u0[k] + h, 20001)
+            obj = tau * (L[k] * (grid - u0[k]) + 0.5 * Qd[k] * (grid - u0[k]) ** 2) + 0.5 * (grid - uh[k]) ** 2
+            assert abs(float(got[k]) - grid[np.argmin(obj)]) < 2e-4
+    n = 0
+    while n < 40:
+        u0 = rng.uniform(-3, 3, 2)
+        M = rng.normal(size=(2, 2))
+        Q = M @ M.T * rng.uniform(0.5, 5)
+        L = rng.uniform(-4, 4, 2)
+        tau = rng.uniform(0.1, 1.0)
+        uh = u0 + rng.uniform(-1, 1, 2)
+        got = np.array([float(v) for v in rf.prox_quadratic(uh[0], uh[1], u0[0], u0[1], L[0], L[1],
+                                                             Q[0, 0], Q[0, 1], Q[1, 1], tau, 1e6)])
+        if np.abs(got - u0).max() > 2.5:
+            continue
+        n += 1
+        g1, g2 = np.meshgrid(np.linspace(u0[0] - 3, u0[0] + 3, 1201), np.linspace(u0[1] - 3, u0[1] + 3, 1201),
+                             indexing="ij")
+        d1, d2 = g1 - u0[0], g2 - u0[1]
+        obj = tau * (L[0] * d1 + L[1] * d2 + 0.5 * (Q[0, 0] * d1 * d1 + 2 * Q[0, 1] * d1 * d2 + Q[1, 1] * d2 * d2)) \
+            + 0.5 * ((g1 - uh[0]) ** 2 + (g2 - uh[1]) ** 2)
+        i = np.unravel_index(np.argmin(obj), obj.shape)
+        assert abs(got[0] - g1[i]) < 1e-2 and abs(got[1] - g2[i]) < 1e-2
 
 
 def test_flow_refine_zero_regularisation(orc):
-    """w = 0, one warp: each component minimises its own quadratic model on
-    [u0 - h, u0 + h] (closed form of Eq. 19 restricted to the box)."""
+    """w = 0: the duals stay 0 and the primal iterates u <- prox(u) of every
+    pixel converge to the minimiser of its own quadratic model where that lies
+    inside the box and Q is well conditioned: Q u = Q u0 - L (np.linalg.solve)."""
     import datagen
     i1, i2, g1, g2 = datagen.flow_pair(30, 20, 8, seed=2)
     c1, c2 = orc.census(i1), orc.census(i2)
     u1 = np.clip(g1, -7, 7).astype(np.float64)
     u2 = np.clip(g2, -7, 7).astype(np.float64)
     r1, r2, _ = rf.flow_refine(c1, c2, u1, u2, 0.0, 0.0, warps=1, iters=400)
-    L1, Q1, L2, Q2 = rf.flow_quadratic(c1, c2, u1, u2, 1.0)
-    for u0, L, Q, r in ((u1, L1, Q1, r1), (u2, L2, Q2, r2)):
-        grid = u0[..., None] + np.linspace(-1, 1, 2001)[None, None, :]
-        obj = L[..., None] * (grid - u0[..., None]) + 0.5 * Q[..., None] * (grid - u0[..., None]) ** 2
-        mn = obj.min(-1)
-        got = L * (r - u0) + 0.5 * Q * (r - u0) ** 2
-        assert np.all(got <= mn + 1e-6)
+    L1, L2, Qa, Qb, Qc = rf.flow_quadratic(c1, c2, u1, u2, 1.0)
+    checked = 0
+    for y in range(u1.shape[0]):
+        for x in range(u1.shape[1]):
+            Q = np.array([[Qa[y, x], Qb[y, x]], [Qb[y, x], Qc[y, x]]])
+            if np.linalg.eigvalsh(Q).min() < 0.5:
+                continue
+            star = np.array([u1[y, x], u2[y, x]]) - np.linalg.solve(Q, [L1[y, x], L2[y, x]])
+            if np.abs(star - [u1[y, x], u2[y, x]]).max() >= 1.0:
+                continue
+            checked += 1
+            assert abs(r1[y, x] - star[0]) < 1e-9 and abs(r2[y, x] - star[1]) < 1e-9
+    assert checked > 20
