@@ -623,6 +623,43 @@ def test_flow_refine_parity(orc, W, H, K, u1, u2, prm):
     assert torch.equal(g1, h1) and torch.equal(g2, h2) and abs(e2 - e) <= 1e-12 * abs(e)
 
 
+@pytest.mark.parametrize("W,H", [(1, 23), (37, 1), (2, 2), (65, 41), (57, 33)])
+def test_refine_degenerate_shapes(orc, W, H):
+    """Refinement on single-row / single-column frames and on frames one pixel
+    past a tile boundary (stereo tile 56 x 32 inner, flow 56 x 16), iteration
+    counts that are not multiples of the 4 iterations per tile launch."""
+    from oracle import refine as orf
+    left, right, _ = datagen.pair("wt-kitti", W, H, 16, seed=W * 31 + H)
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=15, max_iters=2)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(2)
+    u, e = ctx.refine(eps=0.5, delta=2.0, C=5.0, warps=2, iters=9)
+    uo, eo = orf.refine(ctx.cost_volume_tensor().cpu().numpy(), ctx.labels().cpu().numpy(), 3.0, 3.0,
+                        eps=0.5, delta=2.0, C=5.0, warps=2, iters=9)
+    assert np.array_equal(u.cpu().numpy(), uo.astype(np.float32))
+    assert abs(e - eo) <= REFINE_E_RTOL * max(abs(eo), 1.0)
+    _, (g1, g2, fe), (o1, o2, foe) = _flow_refine_case(orc, W, H, 16, -8, -8, dict(C=4.0, warps=2, iters=6))
+    assert np.array_equal(g1.cpu().numpy(), o1.astype(np.float32))
+    assert np.array_equal(g2.cpu().numpy(), o2.astype(np.float32))
+    assert abs(fe - foe) <= REFINE_E_RTOL * max(abs(foe), 1.0)
+
+
+def test_refine_zero_iterations(orc):
+    """iters = 0 (warps of the model only) returns the discrete labelling; warps
+    = 0 likewise; the energy is the oracle's energy of the start point."""
+    from oracle import refine as orf
+    left, right, _ = datagen.pair("wt-kitti", 40, 20, 16, seed=5)
+    ctx = _ctx(width=40, height=20, d_min=0, d_max=15, max_iters=2)
+    ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
+    ctx.solve(2)
+    lab = ctx.labels().cpu().numpy()
+    for warps, iters in ((3, 0), (0, 5)):
+        u, e = ctx.refine(warps=warps, iters=iters)
+        assert np.array_equal(u.cpu().numpy(), lab.astype(np.float32))
+        eo = orf.energy(ctx.cost_volume_tensor().cpu().numpy(), lab.astype(np.float64), 3.0, 3.0, 1.0, 1.0, 4.0)
+        assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
+
+
 def test_flow_refine_c4_full_size(orc):
     """configs[3] (C4): 1242x375, 32x32 window, 4 Dual MM iterations per layer,
     then the continuous refinement (5 warps x 40 iterations)."""
