@@ -1,7 +1,7 @@
 """Digest of an ncu --set full report: headline metrics and the per-opcode
 executed-instruction mix / stall samples from the SASS source page.
 
-  python tools/ncu_digest.py gpurun_out/x.ncu-rep
+  python tools/ncu_digest.py gpurun_out/x.ncu-rep [launch-index]   (reports with several kernels)
 """
 import collections
 import csv
@@ -19,22 +19,32 @@ HEAD = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active
 
 
 def raw(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"] + KSEL, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
 
 
 def sass(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + KSEL,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
-    return hdr, rows[2:]
+    body = []
+    for r in rows[2:]:                      # the first kernel's block only
+        if r and r[0] == "Kernel Name":
+            break
+        body.append(r)
+    return hdr, body
+
+
+KSEL = []
 
 
 def main():
     rep = sys.argv[1]
+    if len(sys.argv) > 2:
+        KSEL.extend(["--print-kernel-base", "function", "--launch-skip", sys.argv[2], "--launch-count", "1"])
     r = raw(rep)
     print(f"# {r.get('Kernel Name', ('?', ''))[0][:160]}\n")
     print("| metric | unit | value |\n|---|---|---|")
@@ -51,6 +61,8 @@ def main():
     sm = hdr.index("Warp Stall Sampling (All Samples)")
     ops, smp = collections.Counter(), collections.Counter()
     for row in data:
+        if len(row) <= max(ie, src, sm):
+            continue
         t = row[src].split()
         if not t:
             continue
