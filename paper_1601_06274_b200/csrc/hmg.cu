@@ -56,11 +56,27 @@ __device__ __forceinline__ int genR(const GenArgs& a, int d) {
     return min(lin, a.c);
 }
 
+// `rows` Msg staging rows of 3 KP ints at base (KP = 32 LPL): the pads
+// [0, KP) and [2 KP, 3 KP) of each hold kBigG so the windowed Msg reads its
+// sources x(b +- d), d < dc <= K, without bounds tests; returns the centre
+// of the first row (the next row's centre is 3 KP further)
+template <int LPL>
+__device__ __forceinline__ int* padded_rows(int* base, int rows, int lane) {
+    constexpr int KP = 32 * LPL;
+    for (int r = 0; r < rows; ++r)
+        for (int k = lane; k < KP; k += 32) {
+            base[r * 3 * KP + k] = kBigG;
+            base[r * 3 * KP + 2 * KP + k] = kBigG;
+        }
+    __syncwarp();
+    return base + KP;
+}
+
 template <int LPL>
 struct GenPass {
     const GenArgs& a;
     int chain, n, lane;
-    int* sx;                     // this warp's shared row [KP]
+    int* sx;                     // this warp's shared row: [KP] at sx, kBigG pads [-KP, 0) and [KP, 2 KP)
     __device__ GenPass(const GenArgs& a_, int chain_, int lane_, int* sx_) : a(a_), chain(chain_), lane(lane_), sx(sx_) {
         n = a.vert ? a.H : a.W;
     }
@@ -89,6 +105,80 @@ struct GenPass {
 #pragma unroll
         for (int e = 0; e < LPL; ++e) arr[base + e] = v[e];
     }
+    // Software-pipelined loads (the passes are latency-bound: one dependent Msg
+    // per node): a node's costs are fetched R steps before use as raw words --
+    // D bytes (first pass) or int32 records -- and expanded only at use, so
+    // the load's latency overlaps the R Msg in between.
+    static constexpr int kRawW = LPL;              // words per lane (D bytes use the first ceil(LPL / 4))
+    template <bool FIRST>
+    __device__ __forceinline__ void ldraw(int p, uint32_t (&r)[kRawW]) const {
+        const size_t base = q(p) * a.KP + lane * LPL;
+        if constexpr (FIRST) {
+            if constexpr (LPL == 8) {
+                const uint2 v = *reinterpret_cast<const uint2*>(a.D + base);
+                r[0] = v.x; r[1] = v.y;
+            } else if constexpr (LPL == 4) {
+                r[0] = *reinterpret_cast<const uint32_t*>(a.D + base);
+            } else if constexpr (LPL == 2) {
+                r[0] = *reinterpret_cast<const uint16_t*>(a.D + base);
+            } else {
+                r[0] = a.D[base];
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) r[e] = (uint32_t)a.src[base + e];
+        }
+    }
+    template <bool FIRST>
+    __device__ __forceinline__ void expand(const uint32_t (&r)[kRawW], int (&F)[LPL]) const {
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            F[e] = FIRST ? (int)((r[e >> 2] >> (8 * (e & 3))) & 0xffu) << a.fbits : (int)r[e];
+            if (lane * LPL + e >= a.K) F[e] = kBigG;
+        }
+    }
+    // two independent Msg (their instructions interleave): x over an edge of
+    // weight omx staged in sx, y over omy staged in sy -- each exactly msg()
+    __device__ __forceinline__ void msg2(int (&x)[LPL], int omx, int (&y)[LPL], int omy, int* sy) const {
+        int lx = kBigG, ly = kBigG;
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            if (lane * LPL + e >= a.K) { x[e] = kBigG; y[e] = kBigG; }
+            lx = min(lx, x[e]);
+            ly = min(ly, y[e]);
+        }
+        const int mx = __reduce_min_sync(0xffffffffu, lx), my = __reduce_min_sync(0xffffffffu, ly);
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) { sx[lane * LPL + e] = x[e]; sy[lane * LPL + e] = y[e]; }
+        __syncwarp();
+        const long long wx = (long long)a.w * omx, wy = (long long)a.w * omy;
+        const int rc = genR(a, a.dc);
+        const int capx = mx + (int)((wx * rc) >> 4), capy = my + (int)((wy * rc) >> 4);
+        int bx[LPL], by[LPL];
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) { bx[e] = min(capx, x[e]); by[e] = min(capy, y[e]); }
+        for (int d = 1; d < a.dc; ++d) {
+            const int rd = genR(a, d);
+            const int vx = (int)((wx * rd) >> 4), vy = (int)((wy * rd) >> 4);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) {
+                const int b = lane * LPL + e;
+                // out-of-range sources read kBigG (pads, labels >= K): never the minimum
+                bx[e] = min(bx[e], sx[b - d] + vx);
+                by[e] = min(by[e], sy[b - d] + vy);
+                bx[e] = min(bx[e], sx[b + d] + vx);
+                by[e] = min(by[e], sy[b + d] + vy);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < LPL; ++e) {
+            const bool in = lane * LPL + e < a.K;
+            x[e] = in ? bx[e] : capx;
+            y[e] = in ? by[e] : capy;
+        }
+        __syncwarp();
+    }
     // x := Msg over an edge of weight om: out(b) = min_a x(a) + V(|a-b|), exact
     __device__ __forceinline__ void msg(int (&x)[LPL], int omw) const {
         int lm = kBigG;
@@ -115,8 +205,8 @@ struct GenPass {
 #pragma unroll
             for (int e = 0; e < LPL; ++e) {
                 const int b = lane * LPL + e;
-                if (b - d >= 0) best[e] = min(best[e], sx[b - d] + v);
-                if (b + d < a.K) best[e] = min(best[e], sx[b + d] + v);
+                best[e] = min(best[e], sx[b - d] + v);
+                best[e] = min(best[e], sx[b + d] + v);
             }
         }
 #pragma unroll
@@ -125,12 +215,22 @@ struct GenPass {
     }
 };
 
-// One level of the hierarchy: one warp per (chain, subchain) task.
+// One level of the hierarchy: one warp per (chain, subchain) task.  The
+// task's two passes (into i from the left, into j from the right) are
+// independent chains of Msg: they run interleaved (msg2), their node costs
+// and edge weights fetched kPre steps ahead (register rings, static slots).
 template <int LPL>
+constexpr int kPre = LPL >= 8 ? 4 : 8;
+template <int LPL>
+constexpr int kPreIter = LPL >= 8 ? 2 : 8;       // three node arrays per slot in the sweep
+
+template <int LPL, bool FIRST>
 __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev, int ntasks) {
+    constexpr int R = kPre<LPL>;
     extern __shared__ int gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* sx = gsm + warp * 32 * LPL;
+    int* sx = padded_rows<LPL>(gsm + warp * 6 * 32 * LPL, 2, lane);
+    int* sy = sx + 3 * 32 * LPL;
     for (int t = blockIdx.x * kGW + warp; t < ntasks; t += gridDim.x * kGW) {
         const int chain = t >> lev, s = t & ((1 << lev) - 1);
         GenPass<LPL> g(a, chain, lane, sx);
@@ -149,27 +249,38 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
             g.ld(a.Lb, lo, pl);
             g.ld(a.Rb, hi, pr);
         }
-        // the two passes, the next node's costs and edge weight loaded one step ahead
-        int Fn[LPL], omn = 16;
-        if (lo < i) { g.ldF(lo, Fn); omn = g.om(lo); }
-        for (int p = lo; p < i; ++p) {               // phi into i from the left (edge p into p+1)
+        // left pass: step u adds F(lo + u) and crosses edge lo + u; right pass:
+        // step u adds F(hi - u) and crosses edge hi - u - 1
+        const int nl = i - lo, nr = hi - j, ns = max(nl, nr);
+        uint32_t rl[R][LPL], rr[R][LPL];
+        int ol[R], orr[R];
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) F[e] = Fn[e];
-            const int om = omn;
-            if (p + 1 < i) { g.ldF(p + 1, Fn); omn = g.om(p + 1); }
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) pl[e] += F[e];
-            g.msg(pl, om);
+        for (int k = 0; k < R; ++k) {
+            if (k < nl) { g.template ldraw<FIRST>(lo + k, rl[k]); ol[k] = g.om(lo + k); }
+            if (k < nr) { g.template ldraw<FIRST>(hi - k, rr[k]); orr[k] = g.om(hi - k - 1); }
         }
-        if (hi > j) { g.ldF(hi, Fn); omn = g.om(hi - 1); }
-        for (int p = hi; p > j; --p) {               // phi into j from the right (edge p-1 into p-1)
+        for (int u0 = 0; u0 < ns; u0 += R) {
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) F[e] = Fn[e];
-            const int om = omn;
-            if (p - 1 > j) { g.ldF(p - 1, Fn); omn = g.om(p - 2); }
+            for (int k = 0; k < R; ++k) {
+                const int u = u0 + k;
+                if (u >= ns) break;
+                int Fl[LPL], Fr[LPL];
+                g.template expand<FIRST>(rl[k], Fl);
+                g.template expand<FIRST>(rr[k], Fr);
+                const int oml = ol[k], omr = orr[k];
+                if (u + R < nl) { g.template ldraw<FIRST>(lo + u + R, rl[k]); ol[k] = g.om(lo + u + R); }
+                if (u + R < nr) { g.template ldraw<FIRST>(hi - u - R, rr[k]); orr[k] = g.om(hi - u - R - 1); }
+                int xl[LPL], xr[LPL];
 #pragma unroll
-            for (int e = 0; e < LPL; ++e) pr[e] += F[e];
-            g.msg(pr, om);
+                for (int e = 0; e < LPL; ++e) { xl[e] = pl[e] + Fl[e]; xr[e] = pr[e] + Fr[e]; }
+                g.msg2(xl, oml, xr, omr, sy);
+                const bool dl = u < nl, dr = u < nr;
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) {
+                    pl[e] = dl ? xl[e] : pl[e];
+                    pr[e] = dr ? xr[e] : pr[e];
+                }
+            }
         }
         // Handshake (Alg.5, literal three Msg; readings R9, R10)
         const int omij = g.om(i);
@@ -285,13 +396,16 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     hmg_ends_kernel<<<148, 256, 0, s>>>(a, chains, n);
     int levels = 0;
     while ((1 << levels) < n) ++levels;          // subchains of length >= 2 exist at levels 0 .. levels-1
-    const int smem = kGW * 32 * LPL * 4;
+    const int smem = 6 * kGW * 32 * LPL * 4;
     for (int lev = 0; lev < levels; ++lev) {
         const long long nt = (long long)chains << lev;
         const int ntasks = (int)nt;
         int grid = (ntasks + kGW - 1) / kGW;
         if (grid > 148 * 16) grid = 148 * 16;
-        hmg_level_kernel<LPL><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
+        if (a.first)
+            hmg_level_kernel<LPL, true><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
+        else
+            hmg_level_kernel<LPL, false><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
     }
     hmg_emit_kernel<LPL, false><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2 + levels;
@@ -302,11 +416,12 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
 // preceded by the far-side messages of the current remainder f - lambda
 // (stored in Lb); lambda (in Rb) += floor(m_i / 2^gshift) with the dynamic
 // min-marginal m_i, the last pass with gamma = 1.
-template <int LPL>
+template <int LPL, bool FIRST>
 __global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chains) {
+    constexpr int R = kPreIter<LPL>;
     extern __shared__ int gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* sx = gsm + warp * 32 * LPL;
+    int* sx = padded_rows<LPL>(gsm + warp * 3 * 32 * LPL, 1, lane);
     for (int ch = blockIdx.x * kGW + warp; ch < chains; ch += gridDim.x * kGW) {
         GenPass<LPL> g(a, ch, lane, sx);
         const int n = g.n;
@@ -322,32 +437,82 @@ __global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chain
 #pragma unroll
             for (int e = 0; e < LPL; ++e) psi[e] = 0;
             g.st(a.Lb, start, psi);
-            for (int i = start - dir; i >= 0 && i < n; i -= dir) {
-                const int src = i + dir;
-                g.ldF(src, F);
-                g.ld(a.Rb, src, lam);
+            {   // far-side messages: step u reads node src = start - dir u, writes i = src - dir
+                // (edge min(src, i)); node data fetched R steps ahead
+                uint32_t rf[R][LPL];
+                int rl[R][LPL], ro[R];
 #pragma unroll
-                for (int e = 0; e < LPL; ++e) psi[e] += F[e] - lam[e];
-                g.msg(psi, g.om(dir > 0 ? i : i - 1));
-                g.st(a.Lb, i, psi);
+                for (int k = 0; k < R; ++k)
+                    if (k < n - 1) {
+                        const int src = start - dir * k;
+                        g.template ldraw<FIRST>(src, rf[k]);
+                        g.ld(a.Rb, src, rl[k]);
+                        ro[k] = g.om(dir > 0 ? src - 1 : src);
+                    }
+                for (int u0 = 0; u0 < n - 1; u0 += R) {
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        const int u = u0 + k;
+                        if (u >= n - 1) break;
+                        g.template expand<FIRST>(rf[k], F);
+#pragma unroll
+                        for (int e = 0; e < LPL; ++e) psi[e] += F[e] - rl[k][e];
+                        const int om = ro[k];
+                        if (u + R < n - 1) {
+                            const int src = start - dir * (u + R);
+                            g.template ldraw<FIRST>(src, rf[k]);
+                            g.ld(a.Rb, src, rl[k]);
+                            ro[k] = g.om(dir > 0 ? src - 1 : src);
+                        }
+                        g.msg(psi, om);
+                        g.st(a.Lb, start - dir * (u + 1), psi);
+                    }
+                }
             }
             int phi[LPL];
 #pragma unroll
             for (int e = 0; e < LPL; ++e) phi[e] = 0;
-            for (int i = dir > 0 ? 0 : n - 1; i >= 0 && i < n; i += dir) {
-                g.ldF(i, F);
-                g.ld(a.Rb, i, lam);
-                g.ld(a.Lb, i, psi);
+            {   // the sweep: step u at node i = i0 + dir u (edge min(i, i + dir) when u < n - 1)
+                const int i0 = dir > 0 ? 0 : n - 1;
+                uint32_t rf[R][LPL];
+                int rl[R][LPL], rp[R][LPL], ro[R];
 #pragma unroll
-                for (int e = 0; e < LPL; ++e) {
-                    const int m = phi[e] + F[e] - lam[e] + psi[e];     // min-marginal of f - lambda at i
-                    lam[e] += sh ? (m >> sh) : m;
-                }
-                g.st(a.Rb, i, lam);
-                if (i + dir >= 0 && i + dir < n) {
+                for (int k = 0; k < R; ++k)
+                    if (k < n) {
+                        const int i = i0 + dir * k;
+                        g.template ldraw<FIRST>(i, rf[k]);
+                        g.ld(a.Rb, i, rl[k]);
+                        g.ld(a.Lb, i, rp[k]);
+                        ro[k] = k < n - 1 ? g.om(dir > 0 ? i : i - 1) : 16;
+                    }
+                for (int u0 = 0; u0 < n; u0 += R) {
 #pragma unroll
-                    for (int e = 0; e < LPL; ++e) phi[e] += F[e] - lam[e];
-                    g.msg(phi, g.om(dir > 0 ? i : i - 1));
+                    for (int k = 0; k < R; ++k) {
+                        const int u = u0 + k;
+                        if (u >= n) break;
+                        const int i = i0 + dir * u;
+                        g.template expand<FIRST>(rf[k], F);
+#pragma unroll
+                        for (int e = 0; e < LPL; ++e) {
+                            lam[e] = rl[k][e];
+                            const int m = phi[e] + F[e] - lam[e] + rp[k][e];   // min-marginal of f - lambda at i
+                            lam[e] += sh ? (m >> sh) : m;
+                        }
+                        const int om = ro[k];
+                        if (u + R < n) {
+                            const int i2 = i0 + dir * (u + R);
+                            g.template ldraw<FIRST>(i2, rf[k]);
+                            g.ld(a.Rb, i2, rl[k]);
+                            g.ld(a.Lb, i2, rp[k]);
+                            ro[k] = u + R < n - 1 ? g.om(dir > 0 ? i2 : i2 - 1) : 16;
+                        }
+                        g.st(a.Rb, i, lam);
+                        if (u < n - 1) {
+#pragma unroll
+                            for (int e = 0; e < LPL; ++e) phi[e] += F[e] - lam[e];
+                            g.msg(phi, om);
+                        }
+                    }
                 }
             }
         }
@@ -357,7 +522,10 @@ __global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chain
 template <int LPL>
 void run_iter(const GenArgs& a, int chains, cudaStream_t s, long long& launches) {
     int grid = (chains + kGW - 1) / kGW;
-    hmg_iter_kernel<LPL><<<grid, kGW * 32, kGW * 32 * LPL * 4, s>>>(a, chains);
+    if (a.first)
+        hmg_iter_kernel<LPL, true><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4, s>>>(a, chains);
+    else
+        hmg_iter_kernel<LPL, false><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4, s>>>(a, chains);
     hmg_emit_kernel<LPL, true><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2;
 }
