@@ -391,13 +391,151 @@ hmg_energy_kernel(const uint8_t* __restrict__ D, const uint8_t* __restrict__ lab
     }
 }
 
+// Leaf blocks: every subchain of level `lev` (<= kGLeaf nodes) is finished
+// on chip by one warp -- the remaining levels of the hierarchy depth first
+// (a pending right part with its boundary messages on a shared-memory stack),
+// then each single node emitted as hmg_emit_kernel does: lambda = L + F + R
+// (R8), record L + R + D 2^F, the node minimum into the bound, last V: the
+// lowest-index argmin label.  The same operations on the same operands as
+// the level kernels + emit (bit-identical); the block's costs and edge
+// weights are staged once, the boundary messages never leave the SM.
+constexpr int kGLeaf = 16;
+
+template <int LPL>   // ints per warp: F rows, 2 padded Msg rows, stack (4 x 2 vectors), edge weights
+constexpr int kLeafInts = kGLeaf * 32 * LPL + 6 * 32 * LPL + 8 * 32 * LPL + kGLeaf;
+
+template <int LPL, bool FIRST>
+__global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, int ntasks) {
+    constexpr int KP = 32 * LPL;
+    extern __shared__ int gsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* wbase = gsm + warp * kLeafInts<LPL>;
+    int* sF = wbase;                                          // [kGLeaf][KP]
+    int* sx = padded_rows<LPL>(wbase + kGLeaf * KP, 2, lane);
+    int* sy = sx + 3 * KP;
+    int* stk = wbase + kGLeaf * KP + 6 * KP;                  // [4][2][KP]: pending (L, R)
+    int* som = stk + 8 * KP;                                  // [kGLeaf] edge weights
+    long long bsum = 0;
+    for (int t = blockIdx.x * kGW + warp; t < ntasks; t += gridDim.x * kGW) {
+        const int chain = t >> lev, s = t & ((1 << lev) - 1);
+        GenPass<LPL> g(a, chain, lane, sx);
+        int lo = 0, hi = g.n - 1;
+        for (int b = lev - 1; b >= 0; --b) {
+            const int mid = lo + (hi - lo + 1) / 2 - 1;
+            if ((s >> b) & 1) lo = mid + 1; else hi = mid;
+        }
+        if (hi < lo) continue;                                // empty (a single node's left part)
+        __syncwarp();
+        for (int p = lo; p <= hi; ++p) {                      // stage the block's costs and weights
+            uint32_t r[LPL];
+            g.template ldraw<FIRST>(p, r);
+            int F[LPL];
+            g.template expand<FIRST>(r, F);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) sF[(p - lo) * KP + lane * LPL + e] = F[e];
+        }
+        if (lane < hi - lo) som[lane] = g.om(lo + lane);
+        int L[LPL], R[LPL];
+        if (lev == 0) {
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) { L[e] = 0; R[e] = 0; }
+        } else {
+            g.ld(a.Lb, lo, L);
+            g.ld(a.Rb, hi, R);
+        }
+        __syncwarp();
+        auto Fof = [&](int p, int e) { return sF[(p - lo) * KP + lane * LPL + e]; };
+        int sl[4], sh[4], depth = 0;                          // pending right parts [sl, sh]
+        int cl = lo, ch = hi;
+        while (true) {
+            if (cl == ch) {                                   // a leaf node: emit (hmg_emit_kernel)
+                const size_t base = g.q(cl) * a.KP + lane * LPL;
+                int lmin = kBigG, arg = 0x7fffffff, lam[LPL];
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) {
+                    const int k = lane * LPL + e;
+                    const int Ds = (int)a.D[base + e] << a.fbits;
+                    const int F = FIRST ? Ds : a.src[base + e];
+                    const int lr = L[e] + R[e];
+                    lam[e] = lr + F;
+                    a.dst[base + e] = k < a.K ? lr + Ds : 0;
+                    if (k < a.K) lmin = min(lmin, lam[e]);
+                }
+                const int m = __reduce_min_sync(0xffffffffu, lmin);
+                bsum += m;
+                if (a.last && a.vert) {
+#pragma unroll
+                    for (int e = LPL - 1; e >= 0; --e)
+                        if (lane * LPL + e < a.K && lam[e] == m) arg = lane * LPL + e;
+                    arg = __reduce_min_sync(0xffffffffu, arg);
+                    if (lane == 0) a.labels[g.q(cl)] = (uint8_t)arg;
+                }
+                if (depth == 0) break;
+                --depth;                                      // the pending right part
+                cl = sl[depth];
+                ch = sh[depth];
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) {
+                    L[e] = stk[(2 * depth) * KP + lane * LPL + e];
+                    R[e] = stk[(2 * depth + 1) * KP + lane * LPL + e];
+                }
+                continue;
+            }
+            const int len = ch - cl + 1, i = cl + len / 2 - 1, j = i + 1;
+            int pl[LPL], pr[LPL];
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) { pl[e] = L[e]; pr[e] = R[e]; }
+            const int nl = i - cl, nr = ch - j, ns = max(nl, nr);
+            for (int u = 0; u < ns; ++u) {                    // the two passes, interleaved
+                const bool dl = u < nl, dr = u < nr;
+                const int pL = dl ? cl + u : cl, pR = dr ? ch - u : ch;
+                int xl[LPL], xr[LPL];
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) { xl[e] = pl[e] + Fof(pL, e); xr[e] = pr[e] + Fof(pR, e); }
+                g.msg2(xl, som[pL - lo], xr, som[max(pR - 1, lo) - lo], sy);
+#pragma unroll
+                for (int e = 0; e < LPL; ++e) {
+                    pl[e] = dl ? xl[e] : pl[e];
+                    pr[e] = dr ? xr[e] : pr[e];
+                }
+            }
+            // Handshake (Alg.5, literal three Msg; readings R9, R10)
+            const int omij = som[i - lo];
+            int pji[LPL], t_[LPL], b_[LPL];
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) pji[e] = Fof(j, e) + pr[e];
+            g.msg(pji, omij);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) t_[e] = (pl[e] + Fof(i, e) - pji[e]) >> 1;
+            g.msg(t_, omij);
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) b_[e] = -t_[e];
+            g.msg(b_, omij);
+            // push [j, ch] with (phi_ij, R); continue with [cl, i] and (L, phi_ji')
+            sl[depth] = j;
+            sh[depth] = ch;
+#pragma unroll
+            for (int e = 0; e < LPL; ++e) {
+                stk[(2 * depth) * KP + lane * LPL + e] = t_[e];
+                stk[(2 * depth + 1) * KP + lane * LPL + e] = R[e];
+                R[e] = b_[e];
+            }
+            ++depth;
+            ch = i;
+        }
+    }
+    if (lane == 0 && bsum != 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.bound), (unsigned long long)bsum);
+}
+
 template <int LPL>
 void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& launches) {
     hmg_ends_kernel<<<148, 256, 0, s>>>(a, chains, n);
-    int levels = 0;
-    while ((1 << levels) < n) ++levels;          // subchains of length >= 2 exist at levels 0 .. levels-1
+    // level kernels down to the first level whose subchains (<= ceil(n / 2^l)
+    // nodes) fit a leaf block; the leaf kernel finishes and emits
+    int lstar = 0;
+    while (((n + (1 << lstar) - 1) >> lstar) > kGLeaf) ++lstar;
     const int smem = 6 * kGW * 32 * LPL * 4;
-    for (int lev = 0; lev < levels; ++lev) {
+    for (int lev = 0; lev < lstar; ++lev) {
         const long long nt = (long long)chains << lev;
         const int ntasks = (int)nt;
         int grid = (ntasks + kGW - 1) / kGW;
@@ -407,8 +545,24 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
         else
             hmg_level_kernel<LPL, false><<<grid, kGW * 32, smem, s>>>(a, lev, ntasks);
     }
-    hmg_emit_kernel<LPL, false><<<148 * 8, kGW * 32, 0, s>>>(a);
-    launches += 2 + levels;
+    {
+        static bool attr = [] {
+            const int b = kGW * kLeafInts<LPL> * 4;
+            cudaFuncSetAttribute(hmg_leaf_kernel<LPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+            cudaFuncSetAttribute(hmg_leaf_kernel<LPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+            return true;
+        }();
+        (void)attr;
+        const int ntasks = chains << lstar;
+        int grid = (ntasks + kGW - 1) / kGW;
+        if (grid > 148 * 8) grid = 148 * 8;
+        const int lsm = kGW * kLeafInts<LPL> * 4;
+        if (a.first)
+            hmg_leaf_kernel<LPL, true><<<grid, kGW * 32, lsm, s>>>(a, lstar, ntasks);
+        else
+            hmg_leaf_kernel<LPL, false><<<grid, kGW * 32, lsm, s>>>(a, lstar, ntasks);
+    }
+    launches += 2 + lstar;
 }
 
 // Iterative minorant (Alg.4, readings R32): one warp per chain,

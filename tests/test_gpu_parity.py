@@ -705,6 +705,9 @@ def _gen_case(orc, kind, W, H, K, pen, ew, iters, w_h=2, w_v=3, d_min=0):
     ("wt-kitti", 120, 36, 64, (0, 16, 3, 64), True),       # eps = 0: flat up to delta (P1-P2-like)
     ("wt-kitti", 90, 21, 128, (12, 16, 1, 96), False),
     ("rd", 33, 17, 40, (16, 16, 0, 64), False),            # classic shape, padded K
+    ("rd", 13, 9, 16, (8, 16, 2, 80), True),               # chains <= 16 nodes: the leaf kernel from the root
+    ("wt-kitti", 150, 24, 256, (8, 16, 2, 80), False),     # 8 labels per lane
+    ("rd", 1, 40, 16, (4, 16, 1, 48), True),               # single-node rows
 ])
 def test_general_parity(orc, kind, W, H, K, pen, ew):
     """hmg.cu (general three-piece penalty, per-edge weights, literal Alg.5)
