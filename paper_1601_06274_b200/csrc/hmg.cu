@@ -219,10 +219,16 @@ struct GenPass {
 // task's two passes (into i from the left, into j from the right) are
 // independent chains of Msg: they run interleaved (msg2), their node costs
 // and edge weights fetched kPre steps ahead (register rings, static slots).
+#ifndef DMM_GPRE
+#define DMM_GPRE 4
+#endif
+#ifndef DMM_GPRE_ITER
+#define DMM_GPRE_ITER 4
+#endif
 template <int LPL>
-constexpr int kPre = LPL >= 8 ? 4 : 8;
+constexpr int kPre = LPL >= 8 ? DMM_GPRE / 2 : DMM_GPRE;
 template <int LPL>
-constexpr int kPreIter = LPL >= 8 ? 2 : 8;       // three node arrays per slot in the sweep
+constexpr int kPreIter = LPL >= 8 ? 2 : DMM_GPRE_ITER;   // three node arrays per slot in the sweep
 
 template <int LPL, bool FIRST>
 __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev, int ntasks) {
