@@ -550,10 +550,13 @@ REFINE_U_TOL = 0.0        # float64 on both sides, same operation order, no FMA 
 REFINE_E_RTOL = 1e-9
 
 
-@pytest.mark.parametrize("W,H,K,eps,delta,C,warps,iters", [(96, 40, 32, 1.0, 1.0, 4.0, 5, 40),
-                                                           (61, 23, 48, 0.5, 2.0, 5.0, 3, 25),
-                                                           (33, 17, 16, 0.25, 1.0, 3.0, 2, 7)])
-def test_refine_parity(orc, W, H, K, eps, delta, C, warps, iters):
+@pytest.mark.parametrize("W,H,K,eps,delta,C,warps,iters,h,tau,sigma", [
+    (96, 40, 32, 1.0, 1.0, 4.0, 5, 40, 1.0, 0.35, 0.35),
+    (61, 23, 48, 0.5, 2.0, 5.0, 3, 25, 1.0, 0.35, 0.35),
+    (33, 17, 16, 0.25, 1.0, 3.0, 2, 7, 1.0, 0.35, 0.35),
+    (70, 45, 32, 0.5, 1.5, 4.5, 3, 13, 0.5, 0.2, 0.6),       # half-label trust region, other steps
+])
+def test_refine_parity(orc, W, H, K, eps, delta, C, warps, iters, h, tau, sigma):
     """dmm_refine (float64, CUDA graph of the PDHG iterations) vs the float64
     oracle (oracle/refine.py) started from the same discrete labelling.  The
     refined u is returned as float32: compared within its rounding."""
@@ -562,10 +565,11 @@ def test_refine_parity(orc, W, H, K, eps, delta, C, warps, iters):
     ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, max_iters=4)
     ctx.cost_volume(torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda())
     ctx.solve(4)
-    u, e = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    u, e = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters, h=h, tau=tau, sigma=sigma)
     D = ctx.cost_volume_tensor().cpu().numpy()
     lab = ctx.labels().cpu().numpy()
-    uo, eo = orf.refine(D, lab, 3.0, 3.0, eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    uo, eo = orf.refine(D, lab, 3.0, 3.0, eps=eps, delta=delta, C=C, warps=warps, iters=iters, h=h, tau=tau,
+                        sigma=sigma)
     du = np.abs(u.cpu().numpy().astype(np.float64) - uo)
     print(f"refine max |du| = {du.max():.3e}, energy {e:.6f} vs {eo:.6f} (rel {abs(e - eo) / abs(eo):.2e})")
     # u is returned in float32: compare with the oracle's float64 u rounded to float32
@@ -573,7 +577,7 @@ def test_refine_parity(orc, W, H, K, eps, delta, C, warps, iters):
     assert abs(e - eo) <= REFINE_E_RTOL * abs(eo)
     # a second call with the same parameters replays the cached graph: same u
     # (the energy's double atomics may add in another order: last-bit only)
-    u2, e2 = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters)
+    u2, e2 = ctx.refine(eps=eps, delta=delta, C=C, warps=warps, iters=iters, h=h, tau=tau, sigma=sigma)
     assert torch.equal(u, u2) and abs(e2 - e) <= 1e-12 * abs(e)
 
 
@@ -610,7 +614,8 @@ def _flow_refine_case(orc, W, H, K, u1_min, u2_min, prm):
 @pytest.mark.parametrize("W,H,K,u1,u2,prm", [
     (77, 45, 32, -16, -16, dict(C=4.0)),
     (61, 23, 16, -8, -3, dict(eps=0.5, delta=2.0, C=5.0, warps=3, iters=25)),
-    (40, 70, 48, -20, -30, dict(eps=0.25, delta=1.0, C=3.0, warps=2, iters=7, tau=0.2, sigma=0.5))])
+    (40, 70, 48, -20, -30, dict(eps=0.25, delta=1.0, C=3.0, warps=2, iters=7, tau=0.2, sigma=0.5)),
+    (66, 50, 32, -16, -16, dict(C=4.0, warps=3, iters=10, h=0.5))])          # half-pixel differences
 def test_flow_refine_parity(orc, W, H, K, u1, u2, prm):
     """dmm_flow_refine (quadratic model of Eq. 19 rebuilt per warp, Eq. 20's
     prox, float64 without FMA) vs oracle.refine.flow_refine from the same two
