@@ -78,6 +78,14 @@ def cpu_model():
     return None
 
 
+def kp_of(K):
+    """Label pitch of the stored cost volume (capi.cu kp_of: 32 x a power of two >= K)."""
+    lpl = 1
+    while 32 * lpl < K:
+        lpl *= 2
+    return 32 * lpl
+
+
 def alg_bytes_compact(W, H, K, iters, frames=1):
     """SURVEY 8(d) algorithmic bytes of the chain-DP half-steps of one step, on
     the lossless compact basis (u16 label spans + one int32 offset per pixel
@@ -374,14 +382,25 @@ def main():
                 "traffic_source": f"profiles/ncu_traffic_{args.config}.json" if tr else None,
                 "share_of_step": hm_ms_per_step / step_ms_prof if step_ms_prof else None,
                 "per_class_ms_per_step": {k: v[0] / prof_steps for k, v in prof.items()}}
+    # the cost-volume pass (north star: "achieved HBM GB/s ... for the cost-volume
+    # and DP passes"): census codes read (2 x 4 B/pixel) + D written (KP B/pixel)
+    cv_ms = prof["cost_volume"][0] / prof_steps
+    if cv_ms > 0:
+        cv_bytes = nf * W * H * (8 + kp_of(K))
+        roofline["cost_volume_pass"] = {"ms_per_step": cv_ms, "bytes_per_step": cv_bytes,
+                                        "achieved": cv_bytes / (cv_ms / 1e3) / 1e9, "unit": "GB/s",
+                                        "frac": cv_bytes / (cv_ms / 1e3) / 1e9 / hbm,
+                                        "note": "popcount / byte-packing bound, not HBM (DESIGN.md cost_kernel)"}
     refine = None
     if args.refine:
         rms = prof["refine"][0] / prof_steps
-        # per PDHG iteration and pixel (one fused kernel, float64): reads u, u0, s1, s2, p_h, p_v,
-        # q_h, q_v and writes u+, p_h+, p_v+, q_h+, q_v+ (13 doubles)
+        # per PDHG iteration and pixel (float64): reads u, u0, s1, s2, p_h, p_v, q_h, q_v and writes
+        # u+, p_h+, p_v+, q_h+, q_v+ (13 doubles) -- the single-iteration sweep's bytes; the
+        # temporally blocked kernel moves them once per 4 iterations, L2-resident
         rbytes = nf * W * H * 8 * 13 * 5 * 40
         refine = {"ms_per_step": rms, "warps": 5, "iters": 40, "achieved_gbs": rbytes / (rms / 1e3) / 1e9,
-                  "note": "state 104 B/pixel is L2-resident; achieved is algorithmic bytes / time (can exceed HBM)"}
+                  "bound": "fp64 issue (DESIGN.md refinement kernels)",
+                  "note": "achieved = one-iteration-sweep bytes / time (exceeds HBM: 4 iterations per launch)"}
 
     # end to end through the public C ABI with host buffers
     e2e = None

@@ -5,7 +5,7 @@
 // memory with a replicated (clamped) border of `radius` pixels (reading R17).
 // cost_kernel: one CTA per 64-pixel tile of a row (any rectangle of the
 // frame: the whole frame, or a rank's row / column band); see below.
-#include "dmm_internal.cuh"
+#include "hm_device.cuh"
 
 namespace dmm {
 
@@ -61,18 +61,22 @@ void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t
 // it can reach (64 + KP - 1) are staged in shared memory; thread (pixel, label
 // group) computes 16 labels of its pixel (consecutive lanes = consecutive
 // pixels: conflict-free code reads) into a padded shared tile (row stride
-// KP + 16 bytes: conflict-free 16-byte stores), which the CTA then copies out
-// row-major with 16-byte coalesced stores (a warp writes 512 contiguous
-// bytes).  Out-of-image samples are a select, not a branch.
+// KP + 16 bytes: conflict-free 16-byte stores), copied out row-major with
+// 16-byte coalesced stores -- or, for KP = 256 rows, one TMA bulk store
+// (cp.async.bulk shared -> global) per pixel (measured: C3 193 -> 133 us; at
+// KP = 128 the 128-byte bulk copies were slower than the store loop).  KP is a
+// template parameter (32 x a power of two: the copy-out index math is shifts).
+// Out-of-image samples are a select, not a branch.
 constexpr int kCostTX = 64;
 
+template <int KP>
 __global__ void __launch_bounds__(256)
 cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ codes_r, size_t code_fstride,
-            int W, int K, int KP, int d_min, int oob, int x0, int y0, int w, uint8_t* __restrict__ D,
-            size_t d_fstride) {
+            int W, int K, int d_min, int oob, int x0, int y0, int w, uint8_t* __restrict__ D, size_t d_fstride) {
+    constexpr int chunks = KP / 16, stride = KP + 16;
     __shared__ uint32_t sl[kCostTX];
-    __shared__ uint32_t sr[kCostTX + 256];
-    __shared__ __align__(16) uint8_t tile[kCostTX * (256 + 16)];
+    __shared__ uint32_t sr[kCostTX + KP];
+    __shared__ __align__(16) uint8_t tile[kCostTX * stride];
     const int tx0 = x0 + blockIdx.x * kCostTX;            // first pixel of the tile (frame x)
     const int y = y0 + blockIdx.y;
     const size_t fo = (size_t)blockIdx.z * code_fstride + (size_t)y * W;
@@ -84,7 +88,6 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
         if (j < npx) sl[j] = codes_l[fo + tx0 + j];
     }
     __syncthreads();
-    const int chunks = KP / 16, stride = KP + 16;
     const int px = threadIdx.x & (kCostTX - 1);
     const int x = tx0 + px;
     const uint32_t cl = sl[px];
@@ -92,7 +95,8 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
     // padded labels (all but the ~KP/64 border tiles of a row when K == KP):
     // per label one shared load, XOR, POPC and a byte-packing IMAD
     const bool fast = base >= 0 && tx0 + kCostTX - 1 - d_min < W && K == KP;
-    for (int c = threadIdx.x / kCostTX; c < chunks; c += blockDim.x / kCostTX) {
+#pragma unroll
+    for (int c = threadIdx.x / kCostTX; c < chunks; c += 256 / kCostTX) {
         const int k0 = 16 * c;
         uint32_t wv[4];
         if (fast) {
@@ -121,12 +125,22 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
         }
         *reinterpret_cast<uint4*>(tile + px * stride + k0) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
     }
-    __syncthreads();
-    uint4* out = reinterpret_cast<uint4*>(D + (size_t)blockIdx.z * d_fstride +
-                                          ((size_t)blockIdx.y * w + (tx0 - x0)) * KP);
-    for (int q = threadIdx.x; q < npx * chunks; q += blockDim.x) {
-        const int p = q / chunks, c = q - p * chunks;
-        out[q] = *reinterpret_cast<const uint4*>(tile + p * stride + 16 * c);
+    uint8_t* out = D + (size_t)blockIdx.z * d_fstride + ((size_t)blockIdx.y * w + (tx0 - x0)) * KP;
+    if constexpr (KP >= 256) {
+        fence_proxy_async();                               // the tile's generic stores -> the async proxy
+        __syncthreads();
+        if (threadIdx.x < npx) {
+            tma_store_s(out + threadIdx.x * KP, (unsigned)__cvta_generic_to_shared(tile + threadIdx.x * stride), KP);
+            bulk_commit();
+            bulk_wait_read();                              // the tile stays valid until read
+        }
+    } else {
+        __syncthreads();
+        uint4* o4 = reinterpret_cast<uint4*>(out);
+        for (int q = threadIdx.x; q < npx * chunks; q += blockDim.x) {
+            const int p = q / chunks, c = q % chunks;      // compile-time power of two: shifts
+            o4[q] = *reinterpret_cast<const uint4*>(tile + p * stride + 16 * c);
+        }
     }
 }
 
@@ -135,7 +149,16 @@ void launch_cost_rect(const uint32_t* codes_l, const uint32_t* codes_r, size_t c
                       cudaStream_t s) {
     if (w <= 0 || h <= 0) return;
     dim3 grid((w + kCostTX - 1) / kCostTX, h, nframes);
-    cost_kernel<<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, KP, d_min, oob, x0, y0, w, D, d_fstride);
+    switch (KP) {
+        case 32: cost_kernel<32><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w, D,
+                                                      d_fstride); break;
+        case 64: cost_kernel<64><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w, D,
+                                                      d_fstride); break;
+        case 128: cost_kernel<128><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w,
+                                                        D, d_fstride); break;
+        default: cost_kernel<256><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w,
+                                                       D, d_fstride); break;
+    }
 }
 
 void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s) {
