@@ -72,12 +72,29 @@ __device__ __forceinline__ int* padded_rows(int* base, int rows, int lane) {
     return base + KP;
 }
 
+// The CTA's table of V values: vt[om * (dc + 1) + d] = floor(w om R(d) / 16)
+// for om in [0, 16], d in [0, dc] (d = dc: the cap value), filled once per
+// kernel -- the Msg reads V(d) with one broadcast shared load instead of
+// evaluating R(d) and a 64-bit product per distance.
+__device__ __forceinline__ int* fill_vtab(int* vt, const GenArgs& a) {
+    const int vs = a.dc + 1;
+    for (int idx = threadIdx.x; idx < 17 * vs; idx += blockDim.x) {
+        const int om = idx / vs, d = idx - om * vs;
+        vt[idx] = (int)((((long long)a.w * om) * genR(a, d)) >> 4);
+    }
+    __syncthreads();
+    return vt;
+}
+inline size_t vtab_bytes(int dc) { return (size_t)17 * (dc + 1) * sizeof(int); }
+
 template <int LPL>
 struct GenPass {
     const GenArgs& a;
     int chain, n, lane;
     int* sx;                     // this warp's shared row: [KP] at sx, kBigG pads [-KP, 0) and [KP, 2 KP)
-    __device__ GenPass(const GenArgs& a_, int chain_, int lane_, int* sx_) : a(a_), chain(chain_), lane(lane_), sx(sx_) {
+    const int* vt;               // the CTA's V table (fill_vtab)
+    __device__ GenPass(const GenArgs& a_, int chain_, int lane_, int* sx_, const int* vt_)
+        : a(a_), chain(chain_), lane(lane_), sx(sx_), vt(vt_) {
         n = a.vert ? a.H : a.W;
     }
     __device__ __forceinline__ size_t q(int p) const {
@@ -152,15 +169,14 @@ struct GenPass {
 #pragma unroll
         for (int e = 0; e < LPL; ++e) { sx[lane * LPL + e] = x[e]; sy[lane * LPL + e] = y[e]; }
         __syncwarp();
-        const long long wx = (long long)a.w * omx, wy = (long long)a.w * omy;
-        const int rc = genR(a, a.dc);
-        const int capx = mx + (int)((wx * rc) >> 4), capy = my + (int)((wy * rc) >> 4);
+        const int* tx = vt + omx * (a.dc + 1);
+        const int* ty = vt + omy * (a.dc + 1);
+        const int capx = mx + tx[a.dc], capy = my + ty[a.dc];
         int bx[LPL], by[LPL];
 #pragma unroll
         for (int e = 0; e < LPL; ++e) { bx[e] = min(capx, x[e]); by[e] = min(capy, y[e]); }
         for (int d = 1; d < a.dc; ++d) {
-            const int rd = genR(a, d);
-            const int vx = (int)((wx * rd) >> 4), vy = (int)((wy * rd) >> 4);
+            const int vx = tx[d], vy = ty[d];
 #pragma unroll
             for (int e = 0; e < LPL; ++e) {
                 const int b = lane * LPL + e;
@@ -192,8 +208,8 @@ struct GenPass {
 #pragma unroll
         for (int e = 0; e < LPL; ++e) sx[lane * LPL + e] = x[e];
         __syncwarp();
-        const long long wo = (long long)a.w * omw;
-        const int cap = m + (int)((wo * genR(a, a.dc)) >> 4);
+        const int* tv = vt + omw * (a.dc + 1);
+        const int cap = m + tv[a.dc];
         int best[LPL];
 #pragma unroll
         for (int e = 0; e < LPL; ++e) best[e] = min(cap, x[e]);
@@ -201,7 +217,7 @@ struct GenPass {
         // distance (warp-uniform), the lane's LPL labels read their two
         // neighbours at distance d from the staged row
         for (int d = 1; d < a.dc; ++d) {
-            const int v = (int)((wo * genR(a, d)) >> 4);
+            const int v = tv[d];
 #pragma unroll
             for (int e = 0; e < LPL; ++e) {
                 const int b = lane * LPL + e;
@@ -237,9 +253,10 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* sx = padded_rows<LPL>(gsm + warp * 6 * 32 * LPL, 2, lane);
     int* sy = sx + 3 * 32 * LPL;
+    const int* vt = fill_vtab(gsm + kGW * 6 * 32 * LPL, a);
     for (int t = blockIdx.x * kGW + warp; t < ntasks; t += gridDim.x * kGW) {
         const int chain = t >> lev, s = t & ((1 << lev) - 1);
-        GenPass<LPL> g(a, chain, lane, sx);
+        GenPass<LPL> g(a, chain, lane, sx, vt);
         int lo = 0, hi = g.n - 1;
         for (int b = lev - 1; b >= 0; --b) {
             const int mid = lo + (hi - lo + 1) / 2 - 1;
@@ -421,10 +438,11 @@ __global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, 
     int* sy = sx + 3 * KP;
     int* stk = wbase + kGLeaf * KP + 6 * KP;                  // [4][2][KP]: pending (L, R)
     int* som = stk + 8 * KP;                                  // [kGLeaf] edge weights
+    const int* vt = fill_vtab(gsm + kGW * kLeafInts<LPL>, a);
     long long bsum = 0;
     for (int t = blockIdx.x * kGW + warp; t < ntasks; t += gridDim.x * kGW) {
         const int chain = t >> lev, s = t & ((1 << lev) - 1);
-        GenPass<LPL> g(a, chain, lane, sx);
+        GenPass<LPL> g(a, chain, lane, sx, vt);
         int lo = 0, hi = g.n - 1;
         for (int b = lev - 1; b >= 0; --b) {
             const int mid = lo + (hi - lo + 1) / 2 - 1;
@@ -540,7 +558,7 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     // nodes) fit a leaf block; the leaf kernel finishes and emits
     int lstar = 0;
     while (((n + (1 << lstar) - 1) >> lstar) > kGLeaf) ++lstar;
-    const int smem = 6 * kGW * 32 * LPL * 4;
+    const int smem = 6 * kGW * 32 * LPL * 4 + (int)vtab_bytes(a.dc);
     for (int lev = 0; lev < lstar; ++lev) {
         const long long nt = (long long)chains << lev;
         const int ntasks = (int)nt;
@@ -553,7 +571,7 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     }
     {
         static bool attr = [] {
-            const int b = kGW * kLeafInts<LPL> * 4;
+            const int b = kGW * kLeafInts<LPL> * 4 + (int)vtab_bytes(256);
             cudaFuncSetAttribute(hmg_leaf_kernel<LPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
             cudaFuncSetAttribute(hmg_leaf_kernel<LPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
             return true;
@@ -562,7 +580,7 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
         const int ntasks = chains << lstar;
         int grid = (ntasks + kGW - 1) / kGW;
         if (grid > 148 * 8) grid = 148 * 8;
-        const int lsm = kGW * kLeafInts<LPL> * 4;
+        const int lsm = kGW * kLeafInts<LPL> * 4 + (int)vtab_bytes(a.dc);
         if (a.first)
             hmg_leaf_kernel<LPL, true><<<grid, kGW * 32, lsm, s>>>(a, lstar, ntasks);
         else
@@ -582,8 +600,9 @@ __global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chain
     extern __shared__ int gsm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* sx = padded_rows<LPL>(gsm + warp * 3 * 32 * LPL, 1, lane);
+    const int* vt = fill_vtab(gsm + kGW * 3 * 32 * LPL, a);
     for (int ch = blockIdx.x * kGW + warp; ch < chains; ch += gridDim.x * kGW) {
-        GenPass<LPL> g(a, ch, lane, sx);
+        GenPass<LPL> g(a, ch, lane, sx, vt);
         const int n = g.n;
         int z[LPL];
 #pragma unroll
@@ -683,9 +702,9 @@ template <int LPL>
 void run_iter(const GenArgs& a, int chains, cudaStream_t s, long long& launches) {
     int grid = (chains + kGW - 1) / kGW;
     if (a.first)
-        hmg_iter_kernel<LPL, true><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4, s>>>(a, chains);
+        hmg_iter_kernel<LPL, true><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
     else
-        hmg_iter_kernel<LPL, false><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4, s>>>(a, chains);
+        hmg_iter_kernel<LPL, false><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
     hmg_emit_kernel<LPL, true><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2;
 }
