@@ -338,9 +338,11 @@ __global__ void hmg_ends_kernel(GenArgs a, int chains, int n) {
     }
 }
 
-// Leaves: lambda = Lb + F + Rb; record Lb + Rb + D*2^F; bound += min lambda;
-// last V: lowest argmin label.  One warp per node (grid-stride).
-template <int LPL, bool DIRECT>
+// Output of the iterative minorant (Alg.4): lambda (in Rb) per node; record
+// lambda - F + D*2^F (the other orientation's input), bound += min lambda,
+// last V: lowest argmin label.  One warp per node (grid-stride).  (The
+// hierarchical path emits from its leaf kernel.)
+template <int LPL>
 __global__ void __launch_bounds__(kGW * 32) hmg_emit_kernel(GenArgs a) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
@@ -354,8 +356,7 @@ __global__ void __launch_bounds__(kGW * 32) hmg_emit_kernel(GenArgs a) {
             const int k = lane * LPL + e;
             const int Ds = (int)a.D[base + e] << a.fbits;
             const int F = a.first ? Ds : a.src[base + e];
-            // hierarchical: lambda = Lb + F + Rb (leaf, R8); iterative: lambda = Rb
-            const int lr = DIRECT ? a.Rb[base + e] - F : a.Lb[base + e] + a.Rb[base + e];
+            const int lr = a.Rb[base + e] - F;
             lam[e] = lr + F;
             a.dst[base + e] = k < a.K ? lr + Ds : 0;
             if (k < a.K) lmin = min(lmin, lam[e]);
@@ -417,7 +418,7 @@ hmg_energy_kernel(const uint8_t* __restrict__ D, const uint8_t* __restrict__ lab
 // Leaf blocks: every subchain of level `lev` (<= kGLeaf nodes) is finished
 // on chip by one warp -- the remaining levels of the hierarchy depth first
 // (a pending right part with its boundary messages on a shared-memory stack),
-// then each single node emitted as hmg_emit_kernel does: lambda = L + F + R
+// then each single node emitted: lambda = L + F + R
 // (R8), record L + R + D 2^F, the node minimum into the bound, last V: the
 // lowest-index argmin label.  The same operations on the same operands as
 // the level kernels + emit (bit-identical); the block's costs and edge
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, 
         int sl[4], sh[4], depth = 0;                          // pending right parts [sl, sh]
         int cl = lo, ch = hi;
         while (true) {
-            if (cl == ch) {                                   // a leaf node: emit (hmg_emit_kernel)
+            if (cl == ch) {                                   // a leaf node: emit
                 const size_t base = g.q(cl) * a.KP + lane * LPL;
                 int lmin = kBigG, arg = 0x7fffffff, lam[LPL];
 #pragma unroll
@@ -705,7 +706,7 @@ void run_iter(const GenArgs& a, int chains, cudaStream_t s, long long& launches)
         hmg_iter_kernel<LPL, true><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
     else
         hmg_iter_kernel<LPL, false><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
-    hmg_emit_kernel<LPL, true><<<148 * 8, kGW * 32, 0, s>>>(a);
+    hmg_emit_kernel<LPL><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2;
 }
 
