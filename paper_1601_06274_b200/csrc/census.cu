@@ -57,24 +57,27 @@ void launch_census(const Layout& L, int frame0, int nframes, int radius, int64_t
 // D[y][x][k] = popc(cL[y][x] ^ cR[y][x - d_min - k]) or oob; pads (k >= K) = 0,
 // over the rectangle [x0, x0 + w) x [y0, y0 + h) of a frame whose codes are
 // full-frame rows of W codes; D rows of the rectangle have pitch w*KP.  One CTA
-// per (64-pixel tile, row, frame): the tile's left codes and the right codes
-// it can reach (64 + KP - 1) are staged in shared memory; thread (pixel, label
-// group) computes 16 labels of its pixel (consecutive lanes = consecutive
-// pixels: conflict-free code reads) into a padded shared tile (row stride
-// KP + 16 bytes: conflict-free 16-byte stores), copied out row-major with
-// 16-byte coalesced stores -- or, for KP = 256 rows, one TMA bulk store
-// (cp.async.bulk shared -> global) per pixel (measured: C3 193 -> 133 us; at
-// KP = 128 the 128-byte bulk copies were slower than the store loop).  KP is a
-// template parameter (32 x a power of two: the copy-out index math is shifts).
-// Out-of-image samples are a select, not a branch.
-constexpr int kCostTX = 64;
+// per (kCostTX-pixel tile, row, frame), one thread per pixel computing all KP
+// labels (two threads per pixel, half each, at KP = 256) (per label: one shared load, XOR, POPC, byte packing; the per-CTA
+// setup is amortised over KP labels per thread): the right codes the tile can
+// reach (kCostTX + KP - 1) are staged in shared memory (consecutive lanes read
+// consecutive codes), the labels go to a padded shared tile (row stride KP + 16
+// bytes: conflict-free 16-byte stores) that leaves with 16-byte coalesced
+// stores -- or, for KP = 256, one TMA bulk store (cp.async.bulk shared ->
+// global) per pixel row.  A thread whose samples are all inside the image
+// (and K = KP) takes the test-free path; the others (the left ~KP pixels of a
+// row, padded K) select oob / 0 per label.  KP is a template parameter.
+constexpr int kCostTX = 128;
 
 template <int KP>
-__global__ void __launch_bounds__(256)
+constexpr int kCostTPP = KP >= 256 ? 2 : 1;    // threads per pixel (each a contiguous half of the labels)
+
+template <int KP>
+__global__ void __launch_bounds__(kCostTX * kCostTPP<KP>)
 cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ codes_r, size_t code_fstride,
             int W, int K, int d_min, int oob, int x0, int y0, int w, uint8_t* __restrict__ D, size_t d_fstride) {
-    constexpr int chunks = KP / 16, stride = KP + 16;
-    __shared__ uint32_t sl[kCostTX];
+    constexpr int chunks = KP / 16, stride = KP + 16, NT = kCostTX * kCostTPP<KP>;
+    constexpr int cpt = chunks / kCostTPP<KP>;             // 16-label chunks per thread
     __shared__ uint32_t sr[kCostTX + KP];
     __shared__ __align__(16) uint8_t tile[kCostTX * stride];
     const int tx0 = x0 + blockIdx.x * kCostTX;            // first pixel of the tile (frame x)
@@ -82,31 +85,29 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
     const size_t fo = (size_t)blockIdx.z * code_fstride + (size_t)y * W;
     const int npx = min(kCostTX, x0 + w - tx0);
     const int base = tx0 - d_min - (KP - 1);               // frame x of sr[0]
-    for (int j = threadIdx.x; j < kCostTX + KP - 1; j += blockDim.x) {
+    for (int j = threadIdx.x; j < kCostTX + KP - 1; j += NT) {
         const int xr = base + j;
         sr[j] = (xr >= 0 && xr < W) ? codes_r[fo + xr] : 0u;
-        if (j < npx) sl[j] = codes_l[fo + tx0 + j];
     }
-    __syncthreads();
-    const int px = threadIdx.x & (kCostTX - 1);
+    const int px = threadIdx.x % kCostTX, part = threadIdx.x / kCostTX;
     const int x = tx0 + px;
-    const uint32_t cl = sl[px];
-    // CTA-uniform fast path: every sample of the tile inside the image and no
-    // padded labels (all but the ~KP/64 border tiles of a row when K == KP):
-    // per label one shared load, XOR, POPC and a byte-packing IMAD
-    const bool fast = base >= 0 && tx0 + kCostTX - 1 - d_min < W && K == KP;
+    const uint32_t cl = px < npx ? codes_l[fo + x] : 0u;
+    __syncthreads();
+    // label k samples x - d_min - k: inside the image for x - d_min - W < k <= x - d_min
+    const bool clean = x - d_min >= KP - 1 && x - d_min < W && K == KP;
+    const int s0 = px + KP - 1;                            // sr index of label 0 (label k at s0 - k)
 #pragma unroll
-    for (int c = threadIdx.x / kCostTX; c < chunks; c += 256 / kCostTX) {
-        const int k0 = 16 * c;
+    for (int cc = 0; cc < cpt; ++cc) {
+        const int k0 = 16 * (part * cpt + cc);
         uint32_t wv[4];
-        if (fast) {
-            const int s0 = px + KP - 1 - k0;          // sr index of label k0 (label k at s0 - (k - k0))
+        if (clean) {
 #pragma unroll
             for (int g = 0; g < 4; ++g) {
-                uint32_t v = __popc(cl ^ sr[s0 - 4 * g - 3]);
-                v = v * 256u + __popc(cl ^ sr[s0 - 4 * g - 2]);
-                v = v * 256u + __popc(cl ^ sr[s0 - 4 * g - 1]);
-                wv[g] = v * 256u + __popc(cl ^ sr[s0 - 4 * g]);
+                const int sg = s0 - k0 - 4 * g;
+                uint32_t v = __popc(cl ^ sr[sg - 3]);
+                v = v * 256u + __popc(cl ^ sr[sg - 2]);
+                v = v * 256u + __popc(cl ^ sr[sg - 1]);
+                wv[g] = v * 256u + __popc(cl ^ sr[sg]);
             }
         } else {
 #pragma unroll
@@ -129,15 +130,16 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
     if constexpr (KP >= 256) {
         fence_proxy_async();                               // the tile's generic stores -> the async proxy
         __syncthreads();
-        if (threadIdx.x < npx) {
-            tma_store_s(out + threadIdx.x * KP, (unsigned)__cvta_generic_to_shared(tile + threadIdx.x * stride), KP);
+        if (part == 0 && px < npx) {
+            tma_store_s(out + px * KP, (unsigned)__cvta_generic_to_shared(tile + px * stride), KP);
             bulk_commit();
             bulk_wait_read();                              // the tile stays valid until read
         }
     } else {
         __syncthreads();
         uint4* o4 = reinterpret_cast<uint4*>(out);
-        for (int q = threadIdx.x; q < npx * chunks; q += blockDim.x) {
+#pragma unroll 4
+        for (int q = threadIdx.x; q < npx * chunks; q += NT) {
             const int p = q / chunks, c = q % chunks;      // compile-time power of two: shifts
             o4[q] = *reinterpret_cast<const uint4*>(tile + p * stride + 16 * c);
         }
@@ -149,16 +151,18 @@ void launch_cost_rect(const uint32_t* codes_l, const uint32_t* codes_r, size_t c
                       cudaStream_t s) {
     if (w <= 0 || h <= 0) return;
     dim3 grid((w + kCostTX - 1) / kCostTX, h, nframes);
+#define DMM_COST_CASE(KPV)                                                                                   \
+    case KPV:                                                                                                \
+        cost_kernel<KPV><<<grid, kCostTX * kCostTPP<KPV>, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, \
+                                                                   oob, x0, y0, w, D, d_fstride);            \
+        break;
     switch (KP) {
-        case 32: cost_kernel<32><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w, D,
-                                                      d_fstride); break;
-        case 64: cost_kernel<64><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w, D,
-                                                      d_fstride); break;
-        case 128: cost_kernel<128><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w,
-                                                        D, d_fstride); break;
-        default: cost_kernel<256><<<grid, 256, 0, s>>>(codes_l, codes_r, code_fstride, W, K, d_min, oob, x0, y0, w,
-                                                       D, d_fstride); break;
+        DMM_COST_CASE(32)
+        DMM_COST_CASE(64)
+        DMM_COST_CASE(128)
+        default: DMM_COST_CASE(256)
     }
+#undef DMM_COST_CASE
 }
 
 void launch_cost(const Layout& L, int frame0, int nframes, int d_min, int oob, cudaStream_t s) {
