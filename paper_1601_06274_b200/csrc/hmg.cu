@@ -238,13 +238,8 @@ struct GenPass {
 #ifndef DMM_GPRE
 #define DMM_GPRE 4
 #endif
-#ifndef DMM_GPRE_ITER
-#define DMM_GPRE_ITER 4
-#endif
 template <int LPL>
 constexpr int kPre = LPL >= 8 ? DMM_GPRE / 2 : DMM_GPRE;
-template <int LPL>
-constexpr int kPreIter = LPL >= 8 ? 2 : DMM_GPRE_ITER;   // three node arrays per slot in the sweep
 
 template <int LPL, bool FIRST>
 __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev, int ntasks) {
@@ -590,108 +585,137 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     launches += 2 + lstar;
 }
 
-// Iterative minorant (Alg.4, readings R32): one warp per chain,
-// `passes` sweeps alternating direction (the first from node 0), each
-// preceded by the far-side messages of the current remainder f - lambda
-// (stored in Lb); lambda (in Rb) += floor(m_i / 2^gshift) with the dynamic
-// min-marginal m_i, the last pass with gamma = 1.
-template <int LPL, bool FIRST>
-__global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chains) {
-    constexpr int R = kPreIter<LPL>;
+// Iterative minorant (Alg.4, readings R32): one CTA of KP threads
+// per chain, one label per thread (the sweeps are one long dependent chain of
+// Msg per chain, so the per-step latency is what counts: a label per thread
+// keeps each Msg's window loop at two shared loads per distance).  `passes`
+// sweeps alternating direction (the first from node 0), each preceded by the
+// far-side messages of the current remainder f - lambda (stored in Lb);
+// lambda (in Rb) += floor(m_i / 2^gshift) with the dynamic min-marginal m_i,
+// the last pass with gamma = 1.  A Msg: the thread stages its value in one of
+// two padded rows (alternating, so one CTA barrier per Msg orders both the
+// row and the warp minima), the CTA minimum gives the cap, then the window.
+// Node costs / Lb / Rb of the next kPreIt steps are fetched ahead.
+constexpr int kPreIt = 4;
+
+template <int KP, bool FIRST>
+__global__ void __launch_bounds__(KP) hmg_iter_kernel(GenArgs a, int chains) {
+    constexpr int NW = KP / 32, R = kPreIt;
     extern __shared__ int gsm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* sx = padded_rows<LPL>(gsm + warp * 3 * 32 * LPL, 1, lane);
-    const int* vt = fill_vtab(gsm + kGW * 3 * 32 * LPL, a);
-    for (int ch = blockIdx.x * kGW + warp; ch < chains; ch += gridDim.x * kGW) {
-        GenPass<LPL> g(a, ch, lane, sx, vt);
-        const int n = g.n;
-        int z[LPL];
+    int* rows = gsm;                                  // 2 x [pad KP | row KP | pad KP]
+    int* wmin = gsm + 6 * KP;                         // 2 x NW warp minima
+    const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+    for (int r = 0; r < 2; ++r) { rows[r * 3 * KP + k] = kBigG; rows[r * 3 * KP + 2 * KP + k] = kBigG; }
+    const int* vt = fill_vtab(gsm + 6 * KP + 2 * NW, a);     // (its barrier also covers the pads)
+    const bool in = k < a.K;
+    int par = 0;
+    auto msg = [&](int x, int om) -> int {            // Msg over an edge of weight om, at label k
+        if (!in) x = kBigG;
+        int* row = rows + par * 3 * KP + KP;
+        row[k] = x;
+        const int mw = __reduce_min_sync(0xffffffffu, x);
+        if (lane == 0) wmin[par * NW + warp] = mw;
+        __syncthreads();
+        int m = wmin[par * NW];
 #pragma unroll
-        for (int e = 0; e < LPL; ++e) z[e] = 0;
-        for (int p = 0; p < n; ++p) g.st(a.Rb, p, z);
+        for (int w = 1; w < NW; ++w) m = min(m, wmin[par * NW + w]);
+        const int* tv = vt + om * (a.dc + 1);
+        const int cap = m + tv[a.dc];
+        int best = min(cap, x);
+#pragma unroll 4
+        for (int d = 1; d < a.dc; ++d) {              // out-of-range sources: kBigG pads / labels >= K
+            const int v = tv[d];
+            best = min(best, row[k - d] + v);
+            best = min(best, row[k + d] + v);
+        }
+        par ^= 1;
+        return in ? best : cap;
+    };
+    const int n = a.vert ? a.H : a.W;
+    const int fbits = a.fbits;
+    const long long pst = a.vert ? a.W : 1;           // node stride of a chain (pixels)
+    for (int ch = blockIdx.x; ch < chains; ch += gridDim.x) {
+        // this thread's label of the chain's node p in the [H][W][KP] arrays: cb + p * est
+        const long long c0 = a.vert ? ch : (long long)ch * a.W;
+        const long long cb = c0 * KP + k, est = pst * KP;
+        const uint8_t* Dp = a.D + cb;
+        const int32_t* Sp = a.src + cb;
+        int32_t* Lp = a.Lb + cb;
+        int32_t* Rp = a.Rb + cb;
+        const uint8_t* Op = a.om ? a.om + c0 : nullptr;
+        auto ldF = [&](int p) -> int {                // raw: D byte (FIRST) or the int32 record
+            return FIRST ? (int)Dp[p * est] : Sp[p * est];
+        };
+        auto F_of = [&](int raw) -> int { return !in ? kBigG : (FIRST ? raw << fbits : raw); };
+        auto om_of = [&](int e) -> int { return Op ? (int)Op[e * pst] : 16; };
+        for (int p = 0; p < n; ++p) Rp[p * est] = 0;
         for (int s = 0; s < a.passes; ++s) {
             const int dir = (s & 1) ? -1 : 1;
             const int sh = s == a.passes - 1 ? 0 : a.gshift;
-            const int start = dir > 0 ? n - 1 : 0;          // far end
-            int psi[LPL], F[LPL], lam[LPL];
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) psi[e] = 0;
-            g.st(a.Lb, start, psi);
+            const int start = dir > 0 ? n - 1 : 0;  // far end
+            int psi = 0;
+            Lp[start * est] = psi;
             {   // far-side messages: step u reads node src = start - dir u, writes i = src - dir
-                // (edge min(src, i)); node data fetched R steps ahead
-                uint32_t rf[R][LPL];
-                int rl[R][LPL], ro[R];
+                int rf[R], rl[R], ro[R];
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                    if (k < n - 1) {
-                        const int src = start - dir * k;
-                        g.template ldraw<FIRST>(src, rf[k]);
-                        g.ld(a.Rb, src, rl[k]);
-                        ro[k] = g.om(dir > 0 ? src - 1 : src);
+                for (int j = 0; j < R; ++j)
+                    if (j < n - 1) {
+                        const int src = start - dir * j;
+                        rf[j] = ldF(src);
+                        rl[j] = Rp[src * est];
+                        ro[j] = om_of(dir > 0 ? src - 1 : src);
                     }
                 for (int u0 = 0; u0 < n - 1; u0 += R) {
 #pragma unroll
-                    for (int k = 0; k < R; ++k) {
-                        const int u = u0 + k;
+                    for (int j = 0; j < R; ++j) {
+                        const int u = u0 + j;
                         if (u >= n - 1) break;
-                        g.template expand<FIRST>(rf[k], F);
-#pragma unroll
-                        for (int e = 0; e < LPL; ++e) psi[e] += F[e] - rl[k][e];
-                        const int om = ro[k];
+                        psi += F_of(rf[j]) - rl[j];
+                        const int om = ro[j];
                         if (u + R < n - 1) {
                             const int src = start - dir * (u + R);
-                            g.template ldraw<FIRST>(src, rf[k]);
-                            g.ld(a.Rb, src, rl[k]);
-                            ro[k] = g.om(dir > 0 ? src - 1 : src);
+                            rf[j] = ldF(src);
+                            rl[j] = Rp[src * est];
+                            ro[j] = om_of(dir > 0 ? src - 1 : src);
                         }
-                        g.msg(psi, om);
-                        g.st(a.Lb, start - dir * (u + 1), psi);
+                        psi = msg(psi, om);
+                        Lp[(start - dir * (u + 1)) * est] = psi;
                     }
                 }
             }
-            int phi[LPL];
-#pragma unroll
-            for (int e = 0; e < LPL; ++e) phi[e] = 0;
+            int phi = 0;
             {   // the sweep: step u at node i = i0 + dir u (edge min(i, i + dir) when u < n - 1)
                 const int i0 = dir > 0 ? 0 : n - 1;
-                uint32_t rf[R][LPL];
-                int rl[R][LPL], rp[R][LPL], ro[R];
+                int rf[R], rl[R], rp[R], ro[R];
 #pragma unroll
-                for (int k = 0; k < R; ++k)
-                    if (k < n) {
-                        const int i = i0 + dir * k;
-                        g.template ldraw<FIRST>(i, rf[k]);
-                        g.ld(a.Rb, i, rl[k]);
-                        g.ld(a.Lb, i, rp[k]);
-                        ro[k] = k < n - 1 ? g.om(dir > 0 ? i : i - 1) : 16;
+                for (int j = 0; j < R; ++j)
+                    if (j < n) {
+                        const int i = i0 + dir * j;
+                        rf[j] = ldF(i);
+                        rl[j] = Rp[i * est];
+                        rp[j] = Lp[i * est];
+                        ro[j] = j < n - 1 ? om_of(dir > 0 ? i : i - 1) : 16;
                     }
                 for (int u0 = 0; u0 < n; u0 += R) {
 #pragma unroll
-                    for (int k = 0; k < R; ++k) {
-                        const int u = u0 + k;
+                    for (int j = 0; j < R; ++j) {
+                        const int u = u0 + j;
                         if (u >= n) break;
                         const int i = i0 + dir * u;
-                        g.template expand<FIRST>(rf[k], F);
-#pragma unroll
-                        for (int e = 0; e < LPL; ++e) {
-                            lam[e] = rl[k][e];
-                            const int m = phi[e] + F[e] - lam[e] + rp[k][e];   // min-marginal of f - lambda at i
-                            lam[e] += sh ? (m >> sh) : m;
-                        }
-                        const int om = ro[k];
+                        const int F = F_of(rf[j]);
+                        int lam = rl[j];
+                        const int m = phi + F - lam + rp[j];      // min-marginal of f - lambda at i
+                        lam += sh ? (m >> sh) : m;
+                        const int om = ro[j];
                         if (u + R < n) {
                             const int i2 = i0 + dir * (u + R);
-                            g.template ldraw<FIRST>(i2, rf[k]);
-                            g.ld(a.Rb, i2, rl[k]);
-                            g.ld(a.Lb, i2, rp[k]);
-                            ro[k] = u + R < n - 1 ? g.om(dir > 0 ? i2 : i2 - 1) : 16;
+                            rf[j] = ldF(i2);
+                            rl[j] = Rp[i2 * est];
+                            rp[j] = Lp[i2 * est];
+                            ro[j] = u + R < n - 1 ? om_of(dir > 0 ? i2 : i2 - 1) : 16;
                         }
-                        g.st(a.Rb, i, lam);
-                        if (u < n - 1) {
-#pragma unroll
-                            for (int e = 0; e < LPL; ++e) phi[e] += F[e] - lam[e];
-                            g.msg(phi, om);
-                        }
+                        Rp[i * est] = lam;
+                        if (u < n - 1) phi = msg(phi + F - lam, om);
                     }
                 }
             }
@@ -701,11 +725,13 @@ __global__ void __launch_bounds__(kGW * 32) hmg_iter_kernel(GenArgs a, int chain
 
 template <int LPL>
 void run_iter(const GenArgs& a, int chains, cudaStream_t s, long long& launches) {
-    int grid = (chains + kGW - 1) / kGW;
+    constexpr int KP = 32 * LPL;
+    const size_t smem = (6 * KP + 2 * (KP / 32)) * sizeof(int) + vtab_bytes(a.dc);
+    int grid = chains < 148 * 16 ? chains : 148 * 16;
     if (a.first)
-        hmg_iter_kernel<LPL, true><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
+        hmg_iter_kernel<KP, true><<<grid, KP, smem, s>>>(a, chains);
     else
-        hmg_iter_kernel<LPL, false><<<grid, kGW * 32, 3 * kGW * 32 * LPL * 4 + vtab_bytes(a.dc), s>>>(a, chains);
+        hmg_iter_kernel<KP, false><<<grid, KP, smem, s>>>(a, chains);
     hmg_emit_kernel<LPL><<<148 * 8, kGW * 32, 0, s>>>(a);
     launches += 2;
 }
