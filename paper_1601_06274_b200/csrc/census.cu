@@ -117,6 +117,7 @@ cost_kernel(const uint32_t* __restrict__ codes_l, const uint32_t* __restrict__ c
                 for (int b = 0; b < 4; ++b) {
                     const int k = k0 + g * 4 + b;
                     const int xr = x - d_min - k;
+                    DMM_CHECK((unsigned)xr >= (unsigned)W || (xr - base >= 0 && xr - base < kCostTX + KP - 1));
                     const uint32_t cst =
                         (unsigned)xr < (unsigned)W ? (uint32_t)__popc(cl ^ sr[xr - base]) : (uint32_t)oob;
                     v |= (k < K ? cst : 0u) << (8 * b);

@@ -144,6 +144,16 @@ void launch_flow_costs(const uint32_t* c1, const uint32_t* c2, int W, int H, int
 #endif
 constexpr int kLeafMax = DMM_CMAX;
 
+// Device-side bounds / invariant checks (assert) for a checking build
+// (DMM_NVCC_EXTRA=-DDMM_DEVICE_CHECKS; compute-sanitizer is not available on
+// the GPU pool): staging counts, stack depths, task ranges, shared indices.
+#ifdef DMM_DEVICE_CHECKS
+#include <cassert>
+#define DMM_CHECK(c) assert(c)
+#else
+#define DMM_CHECK(c) ((void)0)
+#endif
+
 // Encode the V tensor maps of one frame (tmap.cu) into dev (4 x 128 B):
 // records `fv` [H][W] of rec bytes, cost volume D [H][W][KP]; box rows 16 / 8 /
 // 12 / 12.  Returns cudaSuccess or the error of the encode / copy.

@@ -188,6 +188,9 @@ struct Task : Pass<LPL, VERT, PAD, WIN, FIRST> {
             ++cur;
         }
         const int cnt = r_left < kCH ? r_left : kCH;
+        DMM_CHECK(slot >= 0 && slot < kNSlot && cnt >= 1 && cnt <= kCH);
+        DMM_CHECK((r_dir > 0 ? r_start : r_start - cnt + 1) >= 0 &&
+                  (r_dir > 0 ? r_start + cnt : r_start + 1) <= this->n);
         const unsigned sbase = ring + slot * slotB;
         const unsigned bar = mbar + 8 * slot;
         // every run is staged in ascending node order; a backward run is read
@@ -427,6 +430,7 @@ __global__ void __launch_bounds__(NW * 32, kLevMinCTAs) hm2_level_kernel(PassArg
         const int s = t & ((1 << lev) - 1);
         int lo, hi;
         task_bounds(n, lev, s, lo, hi);
+        DMM_CHECK(lo >= 0 && hi < n && hi - lo >= 1);
         const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
         MP<LPL> bnd, spn;
         if (!(s & 1)) {   // left piece: reuse fwd, recompute bwd
@@ -489,6 +493,7 @@ __global__ void __launch_bounds__(NW * 32, kLevMinCTAs) hm2_last_kernel(PassArgs
         const int s = t & ((1 << lev) - 1);
         int lo, hi;
         task_bounds(n, lev, s, lo, hi);
+        DMM_CHECK(lo >= 0 && hi < n && hi - lo + 1 <= 2 * kCMax + 1);
         const int ii = lo + (hi - lo + 1) / 2 - 1, j = ii + 1;
         const bool left = !(s & 1);
         const int s0 = left ? ii : lo, s1 = left ? hi : j;     // staged nodes, ascending
@@ -697,6 +702,7 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
         int lo0, hi0;
         task_bounds(n, lstar, b & (nbl - 1), lo0, hi0);
         const int m = hi0 - lo0 + 1;
+        DMM_CHECK(lo0 >= 0 && hi0 < n && m >= 1 && m <= kCMax);
         const bool box = VERT && h.vtma;          // V: two 2-D tensor boxes of kCMax rows (records, D)
         const unsigned bytes = box ? 2 * kCMax * (SREC + KP) : 2 * m * SREC + (FIRST ? 0 : 2 * m * KP);
         bulk_wait_read();    // the previous block's output bulk stores have read the staging slots
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(kNWL * 32, DMM_LEAF_MINB) hm2_leaf_kernel(Pass
             handshake2<LPL, PAD, WIN>(Fi, bia, bib, Fj, bja, bjb, pl, pr, h.dk);
             // children A = (lo, i, L, phi_ji' = pr), B = (j, hi, phi_ij = pl, R), both >= 2
             // nodes: push B, continue with A
+            DMM_CHECK(sp < kDepth);
             stkJ = (stkJ & ~(((1u << kFB) - 1) << (kFB * sp))) | ((unsigned)j << (kFB * sp));
             stkH = (stkH & ~(((1u << kFB) - 1) << (kFB * sp))) | ((unsigned)hi << (kFB * sp));
             __syncwarp();

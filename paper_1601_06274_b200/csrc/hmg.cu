@@ -258,6 +258,7 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
             if ((s >> b) & 1) lo = mid + 1; else hi = mid;
         }
         if (hi <= lo) continue;                       // single node: nothing to split
+        DMM_CHECK(lo >= 0 && hi < g.n);
         const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
         int pl[LPL], pr[LPL], F[LPL];
         if (lev == 0) {
@@ -445,6 +446,7 @@ __global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, 
             if ((s >> b) & 1) lo = mid + 1; else hi = mid;
         }
         if (hi < lo) continue;                                // empty (a single node's left part)
+        DMM_CHECK(lo >= 0 && hi < g.n && hi - lo + 1 <= kGLeaf);
         __syncwarp();
         for (int p = lo; p <= hi; ++p) {                      // stage the block's costs and weights
             uint32_t r[LPL];
@@ -532,6 +534,7 @@ __global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, 
             for (int e = 0; e < LPL; ++e) b_[e] = -t_[e];
             g.msg(b_, omij);
             // push [j, ch] with (phi_ij, R); continue with [cl, i] and (L, phi_ji')
+            DMM_CHECK(depth < 4);
             sl[depth] = j;
             sh[depth] = ch;
 #pragma unroll
