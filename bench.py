@@ -277,10 +277,20 @@ def main():
     import paper_1601_06274_b200 as dmm
 
     world, rank, local = dist_env()
+    # DMM_BENCH_SAME_GPU=1: a control-flow dry run of the multi-rank path on a
+    # one-GPU box (every rank on cuda:0, gloo for the barrier / max-reduce of
+    # the timings; frames mode has no data-path collective).  Never a
+    # measurement: the ranks share one GPU.
+    same_gpu = os.environ.get("DMM_BENCH_SAME_GPU") == "1" and world > 1
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     c = datagen.CONFIGS[args.config]
     W, H, K, iters = c["W"], c["H"], c["K"], c["iters"]
