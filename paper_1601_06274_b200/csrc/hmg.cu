@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
         int ol[R], orr[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
+            // a pass shorter than the other runs idle steps on unloaded slots: their
+            // weight must still index the V table (their results are discarded)
+            ol[k] = orr[k] = 16;
             if (k < nl) { g.template ldraw<FIRST>(lo + k, rl[k]); ol[k] = g.om(lo + k); }
             if (k < nr) { g.template ldraw<FIRST>(hi - k, rr[k]); orr[k] = g.om(hi - k - 1); }
         }
@@ -419,7 +422,11 @@ hmg_energy_kernel(const uint8_t* __restrict__ D, const uint8_t* __restrict__ lab
 // lowest-index argmin label.  The same operations on the same operands as
 // the level kernels + emit (bit-identical); the block's costs and edge
 // weights are staged once, the boundary messages never leave the SM.
-constexpr int kGLeaf = 16;
+#ifndef DMM_GLEAF
+#define DMM_GLEAF 12          // measured: 8 -> 15.5, 12 -> 15.0, 16 -> 16.3 ms (C2, general penalty)
+#endif
+constexpr int kGLeaf = DMM_GLEAF;
+static_assert(kGLeaf >= 2 && kGLeaf <= 16, "leaf stack: 4 pending right parts");
 
 template <int LPL>   // ints per warp: F rows, 2 padded Msg rows, stack (4 x 2 vectors), edge weights
 constexpr int kLeafInts = kGLeaf * 32 * LPL + 6 * 32 * LPL + 8 * 32 * LPL + kGLeaf;
