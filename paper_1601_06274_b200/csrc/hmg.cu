@@ -34,7 +34,10 @@ void pen_of(const dmm_config& c, int& e1, int& e2, int& delta, int& cc);
 
 namespace {
 
-constexpr int kGW = 4;           // warps per CTA
+#ifndef DMM_GW
+#define DMM_GW 4
+#endif
+constexpr int kGW = DMM_GW;      // warps per CTA
 constexpr int kBigG = 1 << 29;   // padded labels
 
 struct GenArgs {
@@ -565,6 +568,13 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     int lstar = 0;
     while (((n + (1 << lstar) - 1) >> lstar) > kGLeaf) ++lstar;
     const int smem = 6 * kGW * 32 * LPL * 4 + (int)vtab_bytes(a.dc);
+    static bool lattr = [] {          // over 48 KB for large kGW x LPL
+        const int b = 6 * kGW * 32 * LPL * 4 + (int)vtab_bytes(256);
+        cudaFuncSetAttribute(hmg_level_kernel<LPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+        cudaFuncSetAttribute(hmg_level_kernel<LPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+        return true;
+    }();
+    (void)lattr;
     for (int lev = 0; lev < lstar; ++lev) {
         const long long nt = (long long)chains << lev;
         const int ntasks = (int)nt;
