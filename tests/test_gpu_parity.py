@@ -93,6 +93,8 @@ CASES = [
     (7, 1000, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),
     (9, 700, 256, 0, 3, 3, 4, 4, 2, 2, "wt-middlebury"),
     (33, 1000, 200, 0, 2, 3, 3, 4, 2, 2, "wt-middlebury"),   # padded K = 200 -> 256, odd W (self-paired chain)
+    (16384, 3, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),      # maximum width (capi.cu valid: W <= 16384)
+    (3, 16384, 16, 0, 3, 3, 4, 4, 2, 2, "rd"),      # maximum height
 ]
 
 
@@ -628,7 +630,7 @@ def test_flow_refine_parity(orc, W, H, K, u1, u2, prm):
     assert torch.equal(g1, h1) and torch.equal(g2, h2) and abs(e2 - e) <= 1e-12 * abs(e)
 
 
-@pytest.mark.parametrize("W,H", [(1, 23), (37, 1), (2, 2), (65, 41), (57, 33)])
+@pytest.mark.parametrize("W,H", [(1, 23), (37, 1), (2, 2), (65, 41), (57, 33), (16384, 3), (3, 4000)])
 def test_refine_degenerate_shapes(orc, W, H):
     """Refinement on single-row / single-column frames and on frames one pixel
     past a tile boundary (stereo tile 56 x 32 inner, flow 56 x 16), iteration
