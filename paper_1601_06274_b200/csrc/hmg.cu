@@ -327,6 +327,123 @@ __global__ void __launch_bounds__(kGW * 32) hmg_level_kernel(GenArgs a, int lev,
     }
 }
 
+// The top levels (few, long tasks: latency-bound) with one CTA of KP threads
+// per task, one label per thread -- the same task as hmg_level_kernel (its two
+// passes interleaved, then Alg.5's three Msg), each Msg CTA-wide: the
+// thread stages its value in one of two padded rows per pass (alternating, so
+// one barrier per step orders rows and warp minima), the CTA minimum gives the
+// cap, the window is two shared loads per distance.  Node data fetched
+// kPreIt steps ahead.
+constexpr int kPreLv = 4;
+
+template <int KP, bool FIRST>
+__global__ void __launch_bounds__(KP) hmg_level_cta_kernel(GenArgs a, int lev, int ntasks) {
+    constexpr int NW = KP / 32, R = kPreLv;
+    extern __shared__ int gsm[];
+    int* rows = gsm;                                  // [2 parities][2 passes] x [pad KP | row KP | pad KP]
+    int* wmin = gsm + 12 * KP;                        // [2 parities][2 passes][NW]
+    const int k = threadIdx.x, lane = k & 31, warp = k >> 5;
+    for (int r = 0; r < 4; ++r) { rows[r * 3 * KP + k] = kBigG; rows[r * 3 * KP + 2 * KP + k] = kBigG; }
+    const int* vt = fill_vtab(gsm + 12 * KP + 4 * NW, a);
+    const bool in = k < a.K;
+    int par = 0;
+    // Msg of the values x (pass 0) and y (pass 1) over edges of weights ox, oy
+    auto msg2 = [&](int& x, int ox, int& y, int oy) {
+        if (!in) { x = kBigG; y = kBigG; }
+        int* rx = rows + (2 * par) * 3 * KP + KP;
+        int* ry = rows + (2 * par + 1) * 3 * KP + KP;
+        rx[k] = x;
+        ry[k] = y;
+        const int mx = __reduce_min_sync(0xffffffffu, x), my = __reduce_min_sync(0xffffffffu, y);
+        if (lane == 0) { wmin[(2 * par) * NW + warp] = mx; wmin[(2 * par + 1) * NW + warp] = my; }
+        __syncthreads();
+        int m0 = wmin[(2 * par) * NW], m1 = wmin[(2 * par + 1) * NW];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) { m0 = min(m0, wmin[(2 * par) * NW + w]); m1 = min(m1, wmin[(2 * par + 1) * NW + w]); }
+        const int* tx = vt + ox * (a.dc + 1);
+        const int* ty = vt + oy * (a.dc + 1);
+        const int capx = m0 + tx[a.dc], capy = m1 + ty[a.dc];
+        int bx = min(capx, x), by = min(capy, y);
+#pragma unroll 4
+        for (int d = 1; d < a.dc; ++d) {
+            const int vx = tx[d], vy = ty[d];
+            bx = min(bx, rx[k - d] + vx);
+            by = min(by, ry[k - d] + vy);
+            bx = min(bx, rx[k + d] + vx);
+            by = min(by, ry[k + d] + vy);
+        }
+        par ^= 1;
+        x = in ? bx : capx;
+        y = in ? by : capy;
+    };
+    auto msg1 = [&](int& x, int ox) { int y = 0; msg2(x, ox, y, 16); };
+    const int n = a.vert ? a.H : a.W;
+    const int fbits = a.fbits;
+    const long long pst = a.vert ? a.W : 1;
+    for (int t = blockIdx.x; t < ntasks; t += gridDim.x) {
+        const int chain = t >> lev, s = t & ((1 << lev) - 1);
+        int lo = 0, hi = n - 1;
+        for (int b = lev - 1; b >= 0; --b) {
+            const int mid = lo + (hi - lo + 1) / 2 - 1;
+            if ((s >> b) & 1) lo = mid + 1; else hi = mid;
+        }
+        if (hi <= lo) continue;                       // single node: nothing to split
+        const long long c0 = a.vert ? chain : (long long)chain * a.W;
+        const long long cb = c0 * KP + k, est = pst * KP;
+        const uint8_t* Dp = a.D + cb;
+        const int32_t* Sp = a.src + cb;
+        const uint8_t* Op = a.om ? a.om + c0 : nullptr;
+        auto ldF = [&](int p) -> int { return FIRST ? (int)Dp[p * est] : Sp[p * est]; };
+        auto F_of = [&](int raw) -> int { return !in ? kBigG : (FIRST ? raw << fbits : raw); };
+        auto om_of = [&](int e) -> int { return Op ? (int)Op[e * pst] : 16; };
+        const int len = hi - lo + 1, i = lo + len / 2 - 1, j = i + 1;
+        int pl = lev == 0 ? 0 : a.Lb[cb + lo * est];
+        int pr = lev == 0 ? 0 : a.Rb[cb + hi * est];
+        const int nl = i - lo, nr = hi - j, ns = max(nl, nr);
+        int rl[R], rr[R], ol[R], orr[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            ol[q] = orr[q] = 16;                      // idle steps of the shorter pass: a valid weight
+            rl[q] = rr[q] = 0;
+            if (q < nl) { rl[q] = ldF(lo + q); ol[q] = om_of(lo + q); }
+            if (q < nr) { rr[q] = ldF(hi - q); orr[q] = om_of(hi - q - 1); }
+        }
+        // the prefetch cursors: node lo + u + R (left), hi - u - R (right), stepped per step
+        const uint8_t* dL = FIRST ? Dp + (lo + R) * est : nullptr;
+        const uint8_t* dR = FIRST ? Dp + (hi - R) * est : nullptr;
+        const int32_t* sL = FIRST ? nullptr : Sp + (lo + R) * est;
+        const int32_t* sR = FIRST ? nullptr : Sp + (hi - R) * est;
+        const uint8_t* oL = Op ? Op + (lo + R) * pst : nullptr;
+        const uint8_t* oR = Op ? Op + (hi - R - 1) * pst : nullptr;
+        for (int u0 = 0; u0 < ns; u0 += R) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const int u = u0 + q;
+                if (u >= ns) break;
+                int xl = pl + F_of(rl[q]), xr = pr + F_of(rr[q]);
+                const int oml = ol[q], omr = orr[q];
+                if (u + R < nl) { rl[q] = FIRST ? (int)*dL : *sL; ol[q] = oL ? (int)*oL : 16; }
+                if (u + R < nr) { rr[q] = FIRST ? (int)*dR : *sR; orr[q] = oR ? (int)*oR : 16; }
+                if (FIRST) { dL += est; dR -= est; } else { sL += est; sR -= est; }
+                if (Op) { oL += pst; oR -= pst; }
+                msg2(xl, oml, xr, omr);
+                if (u < nl) pl = xl;
+                if (u < nr) pr = xr;
+            }
+        }
+        // Handshake (Alg.5, literal three Msg; readings R9, R10)
+        const int omij = om_of(i);
+        int pji = F_of(ldF(j)) + pr;
+        msg1(pji, omij);                              // phi_ji := Msg(f_j + phi_{j+1,j})
+        int t_ = (pl + F_of(ldF(i)) - pji) >> 1;      // floor(m_i/2 - phi_ji)
+        msg1(t_, omij);                               // phi_ij
+        int b_ = -t_;
+        msg1(b_, omij);                               // phi_ji' := Msg(-phi_ij)
+        a.Rb[cb + i * est] = b_;
+        a.Lb[cb + j * est] = t_;
+    }
+}
+
 // Chain ends: Lb[first] = Rb[last] = 0 (the boundary messages of level 0).
 __global__ void hmg_ends_kernel(GenArgs a, int chains, int n) {
     const int KP = a.KP;
@@ -560,6 +677,11 @@ __global__ void __launch_bounds__(kGW * 32) hmg_leaf_kernel(GenArgs a, int lev, 
     if (lane == 0 && bsum != 0) atomicAdd(reinterpret_cast<unsigned long long*>(a.bound), (unsigned long long)bsum);
 }
 
+#ifndef DMM_CTA_TASKS
+#define DMM_CTA_TASKS 1024
+#endif
+constexpr int kCtaTasks = DMM_CTA_TASKS;          // levels with at most this many tasks: hmg_level_cta_kernel
+
 template <int LPL>
 void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& launches) {
     hmg_ends_kernel<<<148, 256, 0, s>>>(a, chains, n);
@@ -578,6 +700,15 @@ void run_half(const GenArgs& a, int chains, int n, cudaStream_t s, long long& la
     for (int lev = 0; lev < lstar; ++lev) {
         const long long nt = (long long)chains << lev;
         const int ntasks = (int)nt;
+        if (ntasks <= kCtaTasks) {                  // few long tasks: a CTA per task
+            constexpr int KP = 32 * LPL;
+            const size_t cs = (12 * KP + 4 * (KP / 32)) * sizeof(int) + vtab_bytes(a.dc);
+            if (a.first)
+                hmg_level_cta_kernel<KP, true><<<ntasks, KP, cs, s>>>(a, lev, ntasks);
+            else
+                hmg_level_cta_kernel<KP, false><<<ntasks, KP, cs, s>>>(a, lev, ntasks);
+            continue;
+        }
         int grid = (ntasks + kGW - 1) / kGW;
         if (grid > 148 * 16) grid = 148 * 16;
         if (a.first)
