@@ -1,6 +1,8 @@
-// refine.cu -- continuous refinement of the discrete stereo labelling (NEXT-2,
-// SURVEY 8(f)): the non-convex primal-dual method of Sec. 2.4 with
-// the two-slope data approximation of Sec. 3.1, in float64.
+// refine.cu -- continuous refinement of the discrete labelling (NEXT-2, SURVEY
+// 8(f)): the non-convex primal-dual method of Sec. 2.4 with the
+// two-slope data approximation of Sec. 3.1 for stereo, or the
+// quadratic model of Eq. 19 and the prox of Eq. 20 for flow (Sec. 3.2,
+// P:449-467), in float64.
 //
 //   u+ = prox_{tau D~}(u - tau A^T (p - q))            (Eq. cont_iterates, P:306-311,
 //   q+ = prox_{tau R_-^*}(q + tau A u)                   grad A of P:350-355, d = 1)
@@ -13,11 +15,10 @@
 // each: every launch reads one and writes the other, so no thread reads a
 // value another thread of the same launch updates), u0 (expansion point), s1,
 // s2 (slopes); edge arrays are indexed by the edge's first pixel.  The
-// iterations run kHalo at a time in refine_tile_kernel (temporal blocking on
-// chip);
-// the state (112 B/pixel, 52 MB at C2) stays L2-resident across launches.  A
-// warp's launches are captured once into a CUDA graph per (frame, parameters)
-// and replayed.
+// iterations run kHalo at a time in refine_tile_kernel / flow_tile_kernel
+// (temporal blocking on chip); the state (112 B/pixel, 52 MB at C2) stays
+// L2-resident across launches.  A warp's launches are captured once into a
+// CUDA graph per (frame, parameters) and replayed.
 #include <cmath>
 #include <cstring>
 
@@ -52,12 +53,6 @@ __device__ __forceinline__ real d_interp(const uint8_t* Dp, int K, real u) {
     return (1.0 - f) * (real)Dp[k0] + f * (real)Dp[k1];
 }
 
-// prox of step * (w r_{a,b})^* (Eq. pprox)
-__device__ __forceinline__ real prox_conj(real t, real w, real a, real b, real step) {
-    const real aw = a * w, at = fabs(t);
-    const real tp = at <= aw ? t : copysign(fmax(aw, at - b * step), t);
-    return fmin(fmax(tp, -w), w);
-}
 
 __device__ __forceinline__ real r_dc(real t, real eps, real delta, real C) {
     const real at = fabs(t);
@@ -125,7 +120,8 @@ __device__ __forceinline__ real dmax(real a, real b) { return a > b ? a : b; }
 __device__ __forceinline__ real dmin(real a, real b) { return a < b ? a : b; }
 __device__ __forceinline__ real dclip(real v, real lo, real hi) { return dmin(dmax(v, lo), hi); }
 
-// prox_conj with its loop-invariant products hoisted: aw = a * w, bs = b * step
+// prox of step * (w r_{a,b})^* (Eq. pprox) with its loop-invariant
+// products hoisted: aw = a * w, bs = b * step
 __device__ __forceinline__ real prox_conj_h(real t, real w, real aw, real bs) {
     const real at = fabs(t);
     const real tp = at <= aw ? t : copysign(dmax(aw, at - bs), t);
