@@ -261,6 +261,39 @@ def test_c2_full_size(orc):
 
 
 @pytest.mark.slow
+def test_c5_batch_full_size(orc):
+    """configs[4] per GPU at full size in bench.py's launch configuration: 64
+    KITTI-shaped frames (8 distinct pairs, cycled as bench.py does) solved as
+    one batch.  Sampled frames (three distinct pairs, at batch positions 0,
+    9 and 63) element by element against the oracle; every frame equals the
+    other copies of its pair (batch position does not matter) and satisfies
+    the bound <= energy and monotone-history properties."""
+    import os
+    c = datagen.CONFIGS["C5"]
+    W, H, K, iters, nf = c["W"], c["H"], c["K"], c["iters"], c["frames"]
+    pairs = [datagen.pair(c["kind"], W, H, K, seed=s) for s in range(8)]
+    Lh = np.stack([pairs[f % 8][0] for f in range(nf)])
+    Rh = np.stack([pairs[f % 8][1] for f in range(nf)])
+    ctx = _ctx(width=W, height=H, d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4, max_iters=iters, batch=nf)
+    ctx.cost_volume_frames(torch.from_numpy(Lh).cuda(), torch.from_numpy(Rh).cuda())
+    ctx.solve(iters, frame=0, nframes=nf)
+    res = [ctx.result(f) for f in range(nf)]
+    labs = [ctx.labels(f).cpu().numpy() for f in range(nf)]
+    for f in range(nf):
+        e, b, hist = res[f]
+        assert b <= e and all(x <= y for x, y in zip(hist, hist[1:]))
+        if f >= 8:
+            assert res[f] == res[f % 8] and np.array_equal(labs[f], labs[f % 8])
+    nth = max(1, min(16, os.cpu_count() or 1))
+    for f in (0, 9, 63):
+        l, r, _ = pairs[f % 8]
+        o = _run_oracle(orc, l, r, 0, K, 3, 3, 4, 4, iters, nthreads=nth)
+        e, b, hist = res[f]
+        assert np.array_equal(labs[f].astype(np.int32), o["labels"])
+        assert e == o["energy"] and np.array_equal(np.array(hist, np.int64), o["bound_hist"])
+
+
+@pytest.mark.slow
 def test_c3_full_size(orc):
     """configs[2] at full size on one GPU (1500x1000x256, 4 iterations, the
     launch configuration bench.py --config C3 times): complete element-by-
