@@ -225,3 +225,23 @@ def test_flow_refine_zero_regularisation(orc):
             checked += 1
             assert abs(r1[y, x] - star[0]) < 1e-9 and abs(r2[y, x] - star[1]) < 1e-9
     assert checked > 20
+
+
+def test_flow_cost_bilinear_between_integers(orc):
+    """R35: on an edge of the integer grid the cost is the linear interpolation
+    of its two endpoints; at a cell centre the mean of the four corners."""
+    import datagen
+    i1, i2, _, _ = datagen.flow_pair(36, 20, 8, seed=3)
+    c1, c2 = orc.census(i1), orc.census(i2)
+    H, W = c1.shape
+    rng = np.random.default_rng(9)
+    a = rng.integers(-6, 6, size=(H, W))
+    b = rng.integers(-6, 6, size=(H, W))
+    fx = rng.uniform(0, 1, size=(H, W))
+    D = lambda da, db: rf.flow_cost_int(c1, c2, a + da, b + db)   # noqa: E731
+    got = rf.flow_cost_bilinear(c1, c2, a + fx, b.astype(np.float64))
+    assert np.allclose(got, (1 - fx) * D(0, 0) + fx * D(1, 0), atol=1e-12)
+    got = rf.flow_cost_bilinear(c1, c2, a.astype(np.float64), b + fx)
+    assert np.allclose(got, (1 - fx) * D(0, 0) + fx * D(0, 1), atol=1e-12)
+    got = rf.flow_cost_bilinear(c1, c2, a + 0.5, b + 0.5)
+    assert np.allclose(got, (D(0, 0) + D(1, 0) + D(0, 1) + D(1, 1)) / 4, atol=1e-12)
