@@ -6,7 +6,7 @@ flow refinement -- each compared with the oracle exactly as the parity tests
 do.  Configurations the library rejects (DMM_E_RANGE / DMM_E_ARG) are
 skipped and counted.
 
-  python tools/fuzz_parity.py [seconds] [seed]
+  python tools/fuzz_parity.py [seconds] [seed] [scale]   (scale multiplies the W / H ranges)
 """
 import os
 import sys
@@ -24,6 +24,9 @@ import paper_1601_06274_b200 as dmm  # noqa: E402
 from oracle import refine as orf  # noqa: E402
 
 
+SCALE = 1
+
+
 class Skip(Exception):
     """A configuration the library rejects at creation (range / argument checks)."""
 
@@ -36,7 +39,7 @@ def mk(**kw):
 
 
 def classic(rng):
-    W, H = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+    W, H = int(rng.integers(1, 300 * SCALE)), int(rng.integers(1, 200 * SCALE))
     K = int(rng.integers(1, 257))
     d_min = int(rng.integers(-8, 9))
     wh, wv, T = int(rng.integers(0, 9)), int(rng.integers(0, 9)), int(rng.integers(1, 12))
@@ -60,7 +63,7 @@ def classic(rng):
 
 
 def general(rng):
-    W, H = int(rng.integers(1, 200)), int(rng.integers(1, 120))
+    W, H = int(rng.integers(1, 200 * SCALE)), int(rng.integers(1, 120 * SCALE))
     K = int(rng.integers(2, 129))
     e2 = int(rng.integers(1, 33))
     e1 = int(rng.integers(0, e2 + 1))
@@ -90,7 +93,7 @@ def general(rng):
 
 
 def flow(rng):
-    W, H = int(rng.integers(2, 150)), int(rng.integers(2, 90))
+    W, H = int(rng.integers(2, 150 * SCALE)), int(rng.integers(2, 90 * SCALE))
     K = int(rng.choice([16, 32, 48, 64]))
     u1, u2 = int(rng.integers(-K, 5)), int(rng.integers(-K, 5))
     i1, i2, _, _ = datagen.flow_pair(W, H, min(K // 2, 16), seed=int(rng.integers(1 << 30)))
@@ -117,7 +120,7 @@ def flow(rng):
 
 
 def refine(rng):
-    W, H = int(rng.integers(1, 200)), int(rng.integers(1, 120))
+    W, H = int(rng.integers(1, 200 * SCALE)), int(rng.integers(1, 120 * SCALE))
     K = int(rng.integers(2, 129))
     left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=int(rng.integers(1 << 30)))
     ctx = mk(width=W, height=H, d_min=0, d_max=K - 1, max_iters=2)
@@ -136,6 +139,8 @@ def refine(rng):
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    global SCALE
+    SCALE = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     rng = np.random.default_rng(seed)
     oracle.build()
     kinds = [classic, classic, general, flow, refine]
