@@ -2,8 +2,8 @@
 shapes, label ranges and regulariser / penalty / refinement parameters for
 every path -- the classic pair and int32 kernels, the general penalty with
 edge weights, the iterative minorant, flow costs + both layers, stereo and
-flow refinement -- each compared with the oracle exactly as the parity tests
-do.  Configurations the library rejects (DMM_E_RANGE / DMM_E_ARG) are
+flow refinement, ROWCOL band sharding at world 1-5 (lockstep in one process)
+-- each compared with the oracle exactly as the parity tests do.  Configurations the library rejects (DMM_E_RANGE / DMM_E_ARG) are
 skipped and counted.
 
   python tools/fuzz_parity.py [seconds] [seed] [scale]   (scale multiplies the W / H ranges)
@@ -136,6 +136,61 @@ def refine(rng):
     return f"refine {W}x{H}x{K} {prm}"
 
 
+def bands(rng):
+    """ROWCOL band sharding, all ranks in one process (the parity tests'
+    lockstep: every rank's half-step through the C ABI, the bytes of
+    dmm_shard_plan moved between the ranks' workspaces -- data movement only)."""
+    from paper_1601_06274_b200 import sharding
+    world = int(rng.integers(1, 6))
+    W, H = int(rng.integers(world, 160 * SCALE)), int(rng.integers(world, 90 * SCALE))
+    K = int(rng.choice([16, 32, 64, 100, 128, 256]))
+    iters = int(rng.integers(1, 4))
+    kw = dict(d_min=0, d_max=K - 1, w=3, T=4, frac_bits=4, max_iters=iters)
+    left, right, _ = datagen.pair("wt-kitti", W, H, K, seed=int(rng.integers(1 << 30)))
+    cfg = dmm.make_config(W, H, **kw)
+    lt, rt = torch.from_numpy(left).cuda(), torch.from_numpy(right).cuda()
+    ctxs = []
+    for r in range(world):
+        c = mk(width=W, height=H, shard_world=world, **kw)
+        try:
+            c.shard(None, r, world, dmm.SHARD_ROWCOL)
+        except dmm.DmmError as ex:
+            raise Skip(str(ex))
+        c.cost_volume(lt, rt)
+        ctxs.append(c)
+
+    def exchange(phase):
+        plans = [dmm.shard_plan(cfg, r, world, phase) for r in range(world)]
+        for r in range(world):
+            for peer, so, sb, ro, rb in plans[r]:
+                pr = plans[peer][r]
+                ctxs[peer].ws_view(pr[3], sb).copy_(ctxs[r].ws_view(so, sb))
+
+    for t in range(iters):
+        for c in ctxs:
+            c.half_step(t, 0, iters)
+        if world > 1:
+            exchange(0)
+        for c in ctxs:
+            c.half_step(t, 1, iters)
+        if world > 1 and t + 1 < iters:
+            exchange(1)
+    torch.cuda.synchronize()
+    labels = np.zeros((H, W), np.int32)
+    hist = np.zeros(2 * iters, np.int64)
+    for r, c in enumerate(ctxs):
+        boff = dmm.shard_locate(cfg, r, world, dmm.LOC_BOUNDS, 0, 0)
+        hist += c.ws_view(boff, 16 * iters).view(torch.int64).cpu().numpy()
+        c0, c1 = sharding.bands(W, world)[r]
+        off = dmm.shard_locate(cfg, r, world, dmm.LOC_LABEL_V, 0, c0)
+        labels[:, c0:c1] = c.ws_view(off, H * (c1 - c0)).view(H, c1 - c0).cpu().numpy()
+    D = oracle.cost_volume(oracle.census(left), oracle.census(right), 0, K, 12)
+    o = oracle.dmm(D, 3, 3, 4, 4, iters, 8)
+    assert np.array_equal(labels, o["labels"]), "band labels"
+    assert np.array_equal(hist, o["bound_hist"]), "band bounds"
+    return f"bands {W}x{H}x{K} world={world} it={iters}"
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
@@ -143,7 +198,7 @@ def main():
     SCALE = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     rng = np.random.default_rng(seed)
     oracle.build()
-    kinds = [classic, classic, general, flow, refine]
+    kinds = [classic, classic, general, flow, refine, bands]
     t0 = time.time()
     n = skipped = 0
     counts = {}
