@@ -6,7 +6,10 @@ flow refinement, ROWCOL band sharding at world 1-5 (lockstep in one process)
 -- each compared with the oracle exactly as the parity tests do.  Configurations the library rejects (DMM_E_RANGE / DMM_E_ARG) are
 skipped and counted.
 
-  python tools/fuzz_parity.py [seconds] [seed] [scale]   (scale multiplies the W / H ranges)
+  python tests/fuzz_parity.py [seconds] [seed] [scale]   (scale multiplies the W / H ranges)
+
+Test infrastructure (it runs the oracle): lives in tests/; a fixed-count run
+is part of the GPU suite (tests/test_gpu_fuzz.py).
 """
 import os
 import sys
@@ -191,18 +194,18 @@ def bands(rng):
     return f"bands {W}x{H}x{K} world={world} it={iters}"
 
 
-def main():
-    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
-    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+def run(budget: float, seed: int, scale: int = 1, max_cases: int = 1 << 30, verbose: bool = True):
+    """Random cases until `budget` seconds or `max_cases` cases; raises on the
+    first mismatch.  Returns (cases, per-kind counts, rejected)."""
     global SCALE
-    SCALE = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+    SCALE = scale
     rng = np.random.default_rng(seed)
     oracle.build()
     kinds = [classic, classic, general, flow, refine, bands]
     t0 = time.time()
     n = skipped = 0
     counts = {}
-    while time.time() - t0 < budget:
+    while time.time() - t0 < budget and n < max_cases:
         fn = kinds[int(rng.integers(len(kinds)))]
         try:
             desc = fn(rng)
@@ -214,9 +217,17 @@ def main():
             raise
         n += 1
         counts[fn.__name__] = counts.get(fn.__name__, 0) + 1
-        if n <= 5 or n % 25 == 0:
+        if verbose and (n <= 5 or n % 25 == 0):
             print(n, desc, flush=True)
-    print(f"fuzz ok: {n} cases {counts}, {skipped} rejected configurations, {time.time() - t0:.0f} s", flush=True)
+    if verbose:
+        print(f"fuzz ok: {n} cases {counts}, {skipped} rejected configurations, {time.time() - t0:.0f} s", flush=True)
+    return n, counts, skipped
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    run(budget, seed, int(sys.argv[3]) if len(sys.argv) > 3 else 1)
 
 
 if __name__ == "__main__":
