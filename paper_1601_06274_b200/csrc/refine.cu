@@ -349,9 +349,16 @@ __global__ void flow_warp_kernel(RefArgs a1, RefArgs a2, FlowArgs f) {
 // memory, the duals in registers, u (before / after the primal step) and
 // p - q per component and direction in shared memory.  Tile 64 x 24, three
 // pixels per thread.
-constexpr int kFTY = 24, kFTPX = 3, kFOY = kFTY - 2 * kHalo;
+#ifndef DMM_FTY
+#define DMM_FTY 24
+#endif
+#ifndef DMM_FTPX
+#define DMM_FTPX 3
+#endif
+constexpr int kFTY = DMM_FTY, kFTPX = DMM_FTPX, kFOY = kFTY - 2 * kHalo;
 constexpr int kFThreads = kTX * kFTY / kFTPX, kFN = kTX * kFTY;
 constexpr size_t kFSmem = 16 * sizeof(real) * kFN;
+static_assert(kFSmem <= 227 * 1024, "flow tile: shared memory per CTA");   // (measured: 24 x 3 beats 16 x 2, 24 x 2)
 
 __global__ void __launch_bounds__(kFThreads) flow_tile_kernel(RefArgs a1, RefArgs a2, int cur, int nt) {
     extern __shared__ real fsm[];
